@@ -1,0 +1,101 @@
+"""Floating-point storage formats of Table 1 and round-to-nearest-even (oracle).
+
+PAPER.md:37-50 (Table 1) lists fp64, fp32, fp16, bf16 (and q43, excluded by BASELINE).
+Reading G12: the unit roundoffs are the exact powers of two
+u = 2^-(m+1): 2^-53, 2^-24, 2^-11, 2^-8 (Table 1 prints them rounded).
+Reading G16: storage rounding is a SINGLE round-to-nearest-even from float64 directly
+to the target format, subnormals kept, overflow -> +-inf (the range guard in hmatrix.py
+then promotes the block, so no inf is ever stored).
+
+``round_rne`` below is written from the definition ("the representable value nearest to
+x, ties to the one with an even last significand bit") and does not use any library
+conversion; tests pin it against numpy's direct float64->float16/float32 casts and
+against exact rational rounding on constructed near-midpoint inputs.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+FP64, FP32, FP16, BF16 = 0, 1, 2, 3          # tag ids (same numbering as include/hh.h)
+TAG_NAMES = {FP64: "fp64", FP32: "fp32", FP16: "fp16", BF16: "bf16"}
+TAG_BIT = {FP64: 1, FP32: 2, FP16: 4, BF16: 8}  # precision_set bitmask
+BYTES = {FP64: 8, FP32: 4, FP16: 2, BF16: 2}
+BITS = {t: 8 * b for t, b in BYTES.items()}
+
+# (mantissa bits m, e_min, e_max) — Table 1 columns (1-e-m), e_min, e_max
+PARAMS = {
+    FP64: (52, -1022, 1023),
+    FP32: (23, -126, 127),
+    FP16: (10, -14, 15),
+    BF16: (7, -126, 127),
+}
+
+
+def unit_roundoff(tag: int) -> float:
+    """u = 2^-(m+1) (Table 1; exact reading G12)."""
+    m = PARAMS[tag][0]
+    return float(np.ldexp(1.0, -(m + 1)))
+
+
+def x_max(tag: int) -> float:
+    """Largest finite value (2 - 2^-m) * 2^emax (Table 1 column x_max)."""
+    m, _, emax = PARAMS[tag]
+    return float(np.ldexp(2.0 - np.ldexp(1.0, -m), emax))
+
+
+def round_rne(x, tag: int) -> np.ndarray:
+    """Round float64 array ``x`` to the nearest value of format ``tag`` (ties to even).
+
+    Returned as float64 (every value of the four formats is exactly representable in
+    float64).  Definition-based: with E = floor(log2|x|), the spacing of representable
+    numbers around |x| is q = 2^(max(E, e_min) - m); the nearest representable value is
+    rint(|x|/q) * q, where rint rounds half to even (an even integer significand is an
+    even last mantissa bit, also across the binade boundary and in the subnormal range).
+    Values whose rounded magnitude exceeds x_max overflow to +-inf.
+    """
+    x = np.asarray(x, dtype=np.float64)
+    if tag == FP64:
+        return x.copy()
+    m, emin, _ = PARAMS[tag]
+    a = np.abs(x)
+    out = np.zeros_like(a)
+    nz = (a != 0) & np.isfinite(a)
+    _, e = np.frexp(a[nz])            # a = f * 2^e, f in [0.5, 1) -> E = e - 1
+    E = e.astype(np.int64) - 1
+    qexp = np.maximum(E, emin) - m
+    M = np.rint(np.ldexp(a[nz], -qexp))   # exact scaling by a power of two; rint = half-even
+    with np.errstate(over="ignore"):
+        out[nz] = np.ldexp(M, qexp)
+    out[~np.isfinite(a)] = a[~np.isfinite(a)]
+    out[out > x_max(tag)] = np.inf
+    return np.copysign(out, x)
+
+
+def to_storage_bits(x64, tag: int) -> np.ndarray:
+    """Bit patterns of ``round_rne(x, tag)`` as stored in an arena (little-endian words).
+
+    fp64/fp32/fp16 patterns are produced by numpy casts of the already-rounded (hence
+    exactly representable) values; bf16 = the upper 16 bits of the exact float32 value.
+    """
+    r = round_rne(x64, tag)
+    if tag == FP64:
+        return r.view(np.uint64)
+    if tag == FP32:
+        return r.astype(np.float32).view(np.uint32)
+    if tag == FP16:
+        return r.astype(np.float16).view(np.uint16)
+    f32 = r.astype(np.float32).view(np.uint32)
+    return (f32 >> np.uint32(16)).astype(np.uint16)
+
+
+def from_storage_bytes(buf: bytes | np.ndarray, tag: int) -> np.ndarray:
+    """Decode raw little-endian arena bytes of format ``tag`` to exact float64 values."""
+    b = np.frombuffer(buf, dtype=np.uint8) if not isinstance(buf, np.ndarray) else buf.view(np.uint8)
+    if tag == FP64:
+        return b.view("<f8").astype(np.float64)
+    if tag == FP32:
+        return b.view("<f4").astype(np.float64)
+    if tag == FP16:
+        return b.view("<f2").astype(np.float64)
+    hi = b.view("<u2").astype(np.uint32) << np.uint32(16)
+    return hi.view(np.float32).astype(np.float64)

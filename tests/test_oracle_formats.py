@@ -1,0 +1,102 @@
+"""Pins for oracle/formats.py (Table 1, RNE storage rounding).  CPU only."""
+import bisect
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import formats as F
+
+
+def test_unit_roundoffs_match_table1():
+    # PAPER.md:42-45 prints u rounded to 3 significant digits
+    printed = {F.FP64: 1.11e-16, F.FP32: 5.96e-8, F.FP16: 4.88e-4, F.BF16: 3.91e-3}
+    for t, u in printed.items():
+        assert abs(F.unit_roundoff(t) - u) / u < 5e-3
+
+
+def test_xmax_match_table1():
+    # Table 1 prints 1.80e308 (rounded up past the largest double); compare its 1.79e308 floor
+    printed = {F.FP64: 1.79e308, F.FP32: 3.40e38, F.FP16: 6.55e4, F.BF16: 3.39e38}
+    for t, v in printed.items():
+        assert abs(F.x_max(t) - v) / v < 5e-3
+
+
+def test_worked_examples():
+    # SPEC.md:277-278 (derived from Table 1): bf16(0.1) = 0.10009765625, fp16(70000) = inf
+    assert F.round_rne(np.array([0.1]), F.BF16)[0] == 0.10009765625
+    assert np.isinf(F.round_rne(np.array([70000.0]), F.FP16)[0])
+    # fp16 overflow threshold: x_max + half ulp (32) rounds to even = 2^16 -> inf
+    assert F.round_rne(np.array([65519.99]), F.FP16)[0] == 65504.0
+    assert np.isinf(F.round_rne(np.array([65520.0]), F.FP16)[0])
+    assert F.round_rne(np.array([1.0]), F.FP32)[0] == 1.0
+
+
+def _all_values(tag):
+    """Every finite non-negative value of a 16-bit format, sorted, with its bit pattern."""
+    bits = np.arange(0, 1 << 15, dtype=np.uint16)
+    if tag == F.FP16:
+        v = bits.view(np.float16).astype(np.float64)
+    else:
+        v = (bits.astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+    ok = np.isfinite(v)
+    order = np.argsort(v[ok], kind="stable")
+    return v[ok][order], bits[ok][order]
+
+
+@pytest.mark.parametrize("tag", [F.FP16, F.BF16])
+def test_rne_matches_bruteforce_enumeration(tag):
+    """Brute force: nearest of ALL representable values, ties to even last bit (exact
+    rational comparison); inputs constructed on and around every rounding midpoint."""
+    vals, bits = _all_values(tag)
+    rng = np.random.default_rng(7)
+    idx = rng.integers(1, vals.size - 2, size=400)
+    xs = []
+    for i in idx:
+        mid = (vals[i] + vals[i + 1]) / 2          # exact in float64
+        xs += [mid, np.nextafter(mid, 0), np.nextafter(mid, np.inf), vals[i]]
+    xs += list(rng.uniform(0, 2 * vals[-1], 200)) + list(rng.uniform(0, 1e-6, 100))
+    xs = np.array(xs)
+    got = F.round_rne(xs, tag)
+    xmax = F.x_max(tag)
+    half_ulp_top = Fraction(vals[-1]) - Fraction(vals[-2])
+    for x, g in zip(xs, got):
+        fx = Fraction(float(x))
+        if fx >= Fraction(xmax) + half_ulp_top / 2:
+            assert np.isinf(g) or (fx == Fraction(xmax) + half_ulp_top / 2 and np.isinf(g))
+            continue
+        k = bisect.bisect_left(vals.tolist(), float(x))
+        cands = [j for j in (k - 1, k) if 0 <= j < vals.size]
+        best = min(cands, key=lambda j: (abs(Fraction(vals[j]) - fx), int(bits[j]) & 1))
+        assert g == vals[best], (x, g, vals[best])
+
+
+@pytest.mark.parametrize("tag,dt", [(F.FP16, np.float16), (F.FP32, np.float32)])
+def test_rne_matches_numpy_direct_cast(tag, dt):
+    """numpy casts float64->float16/float32 directly with round-half-even (library routine)."""
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(20000) * np.exp2(rng.integers(-30, 20, 20000))
+    vals = x.astype(dt).astype(np.float64)
+    mids = (vals[:-1] + np.nextafter(vals[:-1].astype(dt), np.inf, dtype=dt).astype(np.float64)) / 2
+    xs = np.concatenate([x, mids, np.nextafter(mids, 0), np.nextafter(mids, np.inf)])
+    xs = xs[np.isfinite(xs)]
+    with np.errstate(over="ignore"):
+        ref = xs.astype(dt).astype(np.float64)
+    np.testing.assert_array_equal(F.round_rne(xs, tag), ref)
+
+
+def test_bf16_single_rounding_differs_from_double_rounding():
+    """G16: fp64 -> fp32 -> bf16 double-rounds; the oracle must not."""
+    x = np.array([1.0 + 2.0 ** -8 + 2.0 ** -30])    # just above a bf16 midpoint; fp32 rounds onto it
+    direct = F.round_rne(x, F.BF16)[0]
+    twice = F.round_rne(F.round_rne(x, F.FP32), F.BF16)[0]
+    assert direct == 1.0 + 2.0 ** -7 and twice == 1.0
+
+
+def test_storage_bits_roundtrip():
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(1000)
+    for t in (F.FP64, F.FP32, F.FP16, F.BF16):
+        b = F.to_storage_bits(x, t)
+        back = F.from_storage_bytes(b.tobytes(), t)
+        np.testing.assert_array_equal(back, F.round_rne(x, t))

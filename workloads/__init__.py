@@ -1,0 +1,93 @@
+"""Seeded synthetic workloads shared by the oracle, the tests and bench.py.
+
+This module holds ONLY input generation (points, right-hand sides) and the
+parameter dictionaries of the BASELINE.json configs.  It contains none of the
+method's arithmetic, so both sides of every parity check (the CPU oracle in
+``oracle/`` and the CUDA path in ``paper_2604_09147_b200``) may import it
+without sharing any implementation.
+
+Point sets stand in for the paper's P_square workload (PAPER.md:1090,
+"N particles uniformly distributed within the hypercube [-1,1]^d"); the
+BASELINE configs place them in [0,1]^d, the paper's experiments in [-1,1]^d.
+Seeds: points ``default_rng(1000 + k)``, right-hand sides ``default_rng(2000 + k)``
+for config index k in BASELINE order.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+# kernel ids — identical numbering is part of the C-ABI (include/hh.h)
+K_LOG, K_INV_R, K_INV_R2, K_GAUSS, K_EXP = 0, 1, 2, 3, 4
+KERNEL_NAMES = {K_LOG: "log", K_INV_R: "inv_r", K_INV_R2: "inv_r2", K_GAUSS: "gauss", K_EXP: "exp"}
+
+# precision-set bitmask — identical to include/hh.h
+P_FP64, P_FP32, P_FP16, P_BF16 = 1, 2, 4, 8
+P_MIXED = P_FP64 | P_FP32 | P_FP16 | P_BF16
+SWITCH_NONE = -1
+
+
+def points_uniform(n: int, d: int, seed: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+    """N i.i.d. uniform points in [lo,hi]^d, float64, shape (n, d), row-major."""
+    rng = np.random.default_rng(seed)
+    return np.ascontiguousarray(lo + (hi - lo) * rng.random((n, d)), dtype=np.float64)
+
+
+def points_grid_centres(d: int, L: int) -> np.ndarray:
+    """One point at the centre of every cell of a 2^L-per-axis grid (used by golden
+    partition pins: with n_max=1 the depth rule yields exactly L and no empty cell)."""
+    m = 1 << L
+    axes = [(np.arange(m) + 0.5) / m for _ in range(d)]
+    g = np.meshgrid(*axes, indexing="ij")
+    return np.ascontiguousarray(np.stack([a.ravel() for a in g], axis=1), dtype=np.float64)
+
+
+def rhs(n: int, nrhs: int, seed: int, dist: str) -> np.ndarray:
+    """Right-hand sides, float64, shape (n, nrhs) in Fortran (column-major) order."""
+    rng = np.random.default_rng(seed)
+    if dist == "uniform_pm1":
+        x = rng.uniform(-1.0, 1.0, size=(nrhs, n))
+    elif dist == "uniform_01":
+        x = rng.uniform(0.0, 1.0, size=(nrhs, n))
+    elif dist == "normal":
+        x = rng.standard_normal(size=(nrhs, n))
+    else:
+        raise ValueError(dist)
+    return np.asfortranarray(x.T)
+
+
+# BASELINE.json configs, in order (index k drives the seeds).
+CONFIGS = {
+    "2d_tiny": dict(k=0, N=4096, d=2, kernel=K_LOG, scale=1.0, leaf=64, eta=1.0, s=3,
+                    eps=1e-8, pset=P_MIXED, nrhs=1, xdist="uniform_pm1"),
+    "2d_medium": dict(k=1, N=65536, d=2, kernel=K_LOG, scale=1.0, leaf=64, eta=1.0, s=5,
+                      eps=1e-8, pset=P_MIXED, nrhs=1, xdist="uniform_pm1"),
+    "3d_laplace": dict(k=2, N=262144, d=3, kernel=K_INV_R, scale=1.0, leaf=128, eta=1.0, s=3,
+                       eps=1e-6, pset=P_MIXED, nrhs=1, xdist="normal"),
+    "3d_large": dict(k=3, N=1 << 20, d=3, kernel=K_EXP, scale=0.1, leaf=128, eta=1.0, s=4,
+                     eps=1e-6, pset=P_MIXED, nrhs=1, xdist="normal"),
+    "sweep": dict(k=4, N=262144, d=3, kernel=K_INV_R, scale=1.0, leaf=128, eta=1.0, s=3,
+                  eps=1e-6, pset=P_MIXED, nrhs=1, xdist="normal"),
+}
+SWEEP_SWITCH_LEVELS = [SWITCH_NONE, 2, 3, 4, 0]
+
+# Small parity configs the oracle finishes in seconds; they exercise every storage
+# format (Fig. 8 uses eps=1e-4 and 1e-2 to reach fp16/bf16).
+SMALL_CONFIGS = {
+    "2d_tiny": CONFIGS["2d_tiny"],
+    "2d_fig8_e4": dict(k=10, N=6400, d=2, kernel=K_LOG, scale=1.0, leaf=64, eta=1.0, s=3,
+                       eps=1e-4, pset=P_MIXED, nrhs=1, xdist="uniform_pm1", lo=-1.0, hi=1.0),
+    "2d_fig8_e2": dict(k=11, N=6400, d=2, kernel=K_LOG, scale=1.0, leaf=64, eta=1.0, s=3,
+                       eps=1e-2, pset=P_MIXED, nrhs=1, xdist="uniform_pm1", lo=-1.0, hi=1.0),
+    "3d_small_inv_r": dict(k=12, N=8000, d=3, kernel=K_INV_R, scale=1.0, leaf=128, eta=1.0, s=2,
+                           eps=1e-6, pset=P_MIXED, nrhs=1, xdist="normal"),
+    "3d_small_exp": dict(k=13, N=8000, d=3, kernel=K_EXP, scale=0.1, leaf=64, eta=1.0, s=2,
+                         eps=1e-6, pset=P_MIXED, nrhs=4, xdist="normal"),
+}
+
+
+def make_points(cfg: dict) -> np.ndarray:
+    return points_uniform(cfg["N"], cfg["d"], 1000 + cfg["k"], cfg.get("lo", 0.0), cfg.get("hi", 1.0))
+
+
+def make_rhs(cfg: dict, nrhs: int | None = None) -> np.ndarray:
+    return rhs(cfg["N"], nrhs or cfg["nrhs"], 2000 + cfg["k"], cfg["xdist"])
