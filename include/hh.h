@@ -1,0 +1,203 @@
+/*
+ * hh.h — C-ABI of libhh: adaptive mixed-precision hybrid hierarchical (H_h) matrices on
+ * one NVIDIA B200 (sm_100a).  arxiv 2604.09147 ("Adaptive mixed precision H_h matrices").
+ *
+ * The library builds, on the device, the H_h representation of the kernel matrix
+ *     H_ij = f(||x_i - x_j||_2)                                   (Eq. 5.1)
+ * of N points in R^d, and applies it:  y = H-hat x                (Alg. 3).
+ *
+ * Construction (hh_build) follows
+ *   - the balanced 2^d-tree
+ *   - hybrid admissibility Eq. 3.1: standard below the switch level, weak from it
+ *                                                                  PAPER.md:394-403, 552-557
+ *   - Alg. 1: every admissible block compressed to relative Frobenius accuracy eps
+ *     (rank = truncated-SVD rank), leaf diagonal blocks dense
+ *                                                                  PAPER.md:562-619
+ *   - Alg. 4: ||H~||^2 from the kept singular values
+ *   - Alg. 2 / Eq. 4.4: per-block storage precision, the largest u in the precision set with
+ *     u <= eps / (2^{dl/2} xi), xi = ||H~_IJ||/||H~||
+ * and packs the factors into per-precision HBM arenas (layout: DESIGN.md §4).
+ *
+ * Conventions shared by every entry point
+ *   - Pointers documented as "device" must be cudaMalloc'd (or torch CUDA) memory on the
+ *     current device; "host" pointers are ordinary CPU memory (pinned memory is faster).
+ *   - Arrays are little-endian, float64 unless stated; N x d point arrays are row-major;
+ *     N x nrhs vector blocks are column-major with leading dimension N, ORIGINAL point order.
+ *   - Every call returns hh_status; nothing throws or aborts across the ABI.  On a non-OK
+ *     status hh_last_error() returns a thread-local message.
+ *   - There is no CPU fallback: without a usable CUDA device every call that needs one
+ *     returns HH_ECUDA.
+ */
+#ifndef HH_H
+#define HH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hh_matrix *hh_handle;   /* opaque, library-owned */
+
+typedef enum {
+  HH_OK = 0,
+  HH_EINVAL = 1,        /* invalid argument (see each call) */
+  HH_ENOMEM = 2,        /* device or host allocation failed */
+  HH_ECUDA = 3,         /* CUDA runtime/kernel error, or no usable device */
+  HH_ENUMERIC = 4,      /* non-finite input point / vector / kernel entry */
+  HH_EDEPTH = 5,        /* d*L would exceed 62 bits before every leaf holds <= leaf_size points */
+  HH_EUNSUPPORTED = 6   /* outside what this build supports (e.g. 2^{dL} > 2^26 leaf cells) */
+} hh_status;
+
+/* Kernel functions f(r) (length scale: reading G19).
+ * LOG, INV_R, INV_R2 are singular: H_ii = 0.  GAUSS/EXP: H_ii = 1. */
+typedef enum {
+  HH_K_LOG = 0,     /* log r                    */
+  HH_K_INV_R = 1,   /* 1 / r                    */
+  HH_K_INV_R2 = 2,  /* 1 / r^2                  */
+  HH_K_GAUSS = 3,   /* exp(-r^2 / (2 scale^2))  */
+  HH_K_EXP = 4      /* exp(-r / scale)          */
+} hh_kernel_kind;
+
+typedef struct {
+  int32_t kind;     /* hh_kernel_kind */
+  double scale;     /* length scale for GAUSS / EXP; ignored otherwise */
+} hh_kernel;
+
+/* precision_set bitmask (Table 1); FP64 (the working precision) is mandatory. */
+enum { HH_P_FP64 = 1u, HH_P_FP32 = 2u, HH_P_FP16 = 4u, HH_P_BF16 = 8u };
+/* tag ids used in exported tables */
+enum { HH_TAG_FP64 = 0, HH_TAG_FP32 = 1, HH_TAG_FP16 = 2, HH_TAG_BF16 = 3 };
+/* OR into precision_set: compute ranks / tags / norms / byte ledger only, store no factors
+ * (hh_matvec then returns HH_EINVAL).  Used for storage ratios of configurations that do
+ * not fit in HBM (uniform-fp64 H_s at N = 2^20). */
+#define HH_LEDGER_ONLY (1u << 16)
+
+/* switch_level: 0..L is Eq. 3.1 read literally (0 = HODLR); HH_SWITCH_NONE = pure H_s
+ * (Alg. 1 with ell = L: dense leaf neighbours; in mixed precision a leaf neighbour is stored
+ * low-rank iff that is smaller in bits). */
+#define HH_SWITCH_NONE (-1)
+
+/* Block kinds (exported tables) */
+enum { HH_KIND_FAR = 0, HH_KIND_NBR = 1, HH_KIND_SIB = 2, HH_KIND_LNBR = 3, HH_KIND_DIAG = 4 };
+enum { HH_STORE_LR = 0, HH_STORE_DENSE = 1 };
+
+/*
+ * hh_build — construct H-hat on the device.
+ *   points        device, N x d row-major float64, finite.  Read during the call only.
+ *   N, d          N >= 1, 1 <= d <= 3 in this build (HH_EUNSUPPORTED otherwise).
+ *   kernel        see hh_kernel.
+ *   eps           target accuracy, 2^-53 < eps < 1 ("u < eps").
+ *   eta           admissibility parameter > 0 (Eq. 2.1); eta^2 within 1e-12 of an
+ *                 integer is snapped to it.
+ *   leaf_size     n_max >= 1: depth L = smallest L with every leaf holding <= n_max points.
+ *   switch_level  0..L, or HH_SWITCH_NONE.  > L -> HH_EINVAL.
+ *   precision_set bitmask of HH_P_*, must contain HH_P_FP64; may OR HH_LEDGER_ONLY.
+ *   cuda_stream   cudaStream_t (NULL = legacy default stream).  hh_build synchronises it.
+ *   out           receives the handle on HH_OK (unchanged otherwise).
+ * Errors: HH_EINVAL (bad argument), HH_ENUMERIC (non-finite point or kernel entry, e.g.
+ * log of a zero distance between distinct points is mapped to 0 and counted — not an
+ * error — but an overflowing entry is), HH_EDEPTH, HH_ENOMEM (arenas exceed free HBM),
+ * HH_ECUDA.
+ */
+hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel, double eps,
+                   double eta, int32_t leaf_size, int32_t switch_level, uint32_t precision_set,
+                   void *cuda_stream, hh_handle *out);
+
+/*
+ * hh_matvec — y = H-hat x (Alg. 3), fp64 working precision.
+ *   x      device, N x nrhs column-major (ld = N), original point order.  Not modified.
+ *   y      device, same layout; overwritten; must not overlap x.
+ *   nrhs   >= 1 (processed in chunks of <= 16 columns).
+ *   stream cudaStream_t; the call only enqueues work (asynchronous w.r.t. the host).
+ * The result is bitwise reproducible: no atomics, fixed summation order.
+ * Concurrent calls on one handle are not allowed (shared workspace).
+ * Errors: HH_EINVAL (NULL pointers, nrhs < 1, x == y, ledger-only handle), HH_ECUDA.
+ */
+hh_status hh_matvec(hh_handle H, const double *x, double *y, int32_t nrhs, void *cuda_stream);
+
+/*
+ * hh_matvec_host — same product with HOST x and y: copies x host->device, runs hh_matvec
+ * and copies y device->host on `stream`, then synchronises it (the end-to-end path).
+ */
+hh_status hh_matvec_host(hh_handle H, const double *x_host, double *y_host, int32_t nrhs,
+                         void *cuda_stream);
+
+/* Summary of a built handle (always available, host memory, filled by hh_info). */
+typedef struct {
+  int32_t d, L, switch_level, kernel_kind;
+  int64_t N;
+  double eta, eps, kernel_scale;
+  uint32_t precision_set;
+  int32_t ledger_only;
+  int64_t n_cells;            /* 2^{dL} leaf cells (empty ones included) */
+  int64_t nblocks;            /* all blocks, incl. leaf diagonals, canonical order */
+  int64_t n_lowrank, n_dense;
+  int64_t total_rank;         /* sum of ranks = length of the z workspace */
+  double norm2;               /* ||H~||_F^2 (Alg. 4) */
+  int64_t w_bytes[4];         /* W arena sizes per tag (padded) */
+  int64_t u_bytes[4];         /* U arena sizes per tag (padded) */
+  int64_t d_bytes;            /* dense fp64 arena size (padded) */
+  int64_t stored_bytes;       /* algorithmic: sum p(|I|+|J|) bytes(tag) + sum |I||J| 8 */
+  int64_t stored_bytes_tag[5];/* the same split by tag 0..3 and 4 = dense */
+  int64_t padded_bytes;       /* bytes actually streamed by a matvec (arenas incl. padding) */
+  int32_t c_far, c_nbr, c_sib;/* measured sparsity constants (max blocks per target) */
+  int64_t n_fallback, n_promoted, n_coincident, n_retry;
+  double build_seconds;
+} hh_info_t;
+
+hh_status hh_info(hh_handle H, hh_info_t *info);
+
+/* Exported block record (canonical order: level, tgt, src). */
+typedef struct {
+  int64_t tgt, src;           /* Morton codes of target / source cluster at `level` */
+  int64_t zoff;               /* offset in z (low-rank), -1 otherwise */
+  int64_t w_off;              /* byte offset in W[tag] (rank > 0), -1 otherwise */
+  int64_t ucol;               /* first column inside the target's leaf streams, -1 otherwise */
+  int64_t d_off;              /* byte offset in the dense arena (dense blocks), -1 otherwise */
+  double nb2;                 /* ||H~_b||_F^2 = sum of kept sigma^2 (low-rank) */
+  double tot;                 /* ||H_b||_F^2 (computed from the entries) */
+  double maxabs;              /* max |entry| over the unrounded factors */
+  int32_t rank;
+  uint8_t level, kind, tag, storage;
+} hh_block_t;
+
+/*
+ * hh_export — copy tables and arena bytes to host memory.
+ * Two-call protocol: call with every pointer NULL to get sizes via hh_info (or read
+ * out->info); then set the pointers you want and call again.  Each pointer may be NULL
+ * (skipped).  Arena windows: `arena` selects 0..3 = W[tag], 4..7 = U[tag], 8 = dense,
+ * bytes [arena_off, arena_off + arena_len) are copied to arena_dst.
+ */
+typedef struct {
+  hh_info_t info;             /* always filled */
+  int32_t *perm;              /* [N]   tree position -> original index */
+  int64_t *leaf_start;        /* [n_cells + 1] */
+  hh_block_t *blocks;         /* [nblocks] */
+  int64_t *u_leaf_off;        /* [4 * (n_cells + 1)] byte offsets of leaf streams per tag */
+  int64_t *d_leaf_off;        /* [n_cells + 1] */
+  int32_t arena;
+  int64_t arena_off, arena_len;
+  void *arena_dst;
+} hh_export_t;
+
+hh_status hh_export(hh_handle H, hh_export_t *out);
+
+/* hh_free — release every device and host resource of the handle (NULL is a no-op). */
+hh_status hh_free(hh_handle H);
+
+/* Thread-local message for the last non-OK status on this thread ("" if none). */
+const char *hh_last_error(void);
+
+/* Test hook: the device storage-rounding routine of `tag` (HH_TAG_FP32/FP16/BF16) applied to
+ * n host doubles; host_bits receives the target bit patterns (RNE, single rounding, G16). */
+hh_status hh_selftest_round(const double *host_in, int64_t n, int32_t tag, uint32_t *host_bits);
+
+/* Number of kernels the library enqueued since load (launch accounting for bench.py). */
+int64_t hh_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HH_H */

@@ -1,0 +1,376 @@
+// api.cpp — the C-ABI (include/hh.h): argument validation, build orchestration, export.
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "build.h"
+
+namespace hh {
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches += n; }
+
+namespace {
+thread_local std::string g_err;
+
+hh_status fail(hh_status s, const std::string &m) {
+  g_err = m;
+  return s;
+}
+
+constexpr int KMAX = 512;
+
+__global__ void k_round(const double *in, int64_t n, int tag, uint32_t *out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = tag == TAG_FP32 ? to_fp32_bits(in[i]) : tag == TAG_FP16 ? to_fp16_bits(in[i]) : to_bf16_bits(in[i]);
+}
+
+__global__ void k_leaf_of(const int64_t *leaf_start, int64_t ncell, int32_t *leaf_of) {
+  for (int64_t R = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; R < ncell; R += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t t = leaf_start[R]; t < leaf_start[R + 1]; ++t) leaf_of[t] = (int32_t)R;
+}
+
+size_t workspace_budget() {
+  size_t fr = 0, tot = 0;
+  HH_CUDA(cudaMemGetInfo(&fr, &tot));
+  size_t b = fr / 3;
+  return std::max<size_t>(std::min<size_t>(b, (size_t)24 << 30), (size_t)256 << 20);
+}
+
+void compress_all(hh_matrix *H, const double *pts, const std::vector<int64_t> &lr, cudaStream_t st) {
+  // pass 1 with adaptive sketch width: k0 per (level, kind) class from the ranks seen so far
+  const size_t nb = H->level.size();
+  H->rank.assign(nb, 0);
+  H->kfinal.assign(nb, 0);
+  H->nb2.assign(nb, 0.0);
+  H->maxabs.assign(nb, 0.0);
+  std::vector<int> kest(64 * 8, 32);
+  std::vector<CompressJob> jobs;
+  size_t pos = 0;
+  const size_t batch = 16384;
+  int64_t retries = 0;
+  std::vector<CompressJob> retry;
+  std::vector<CompressResult> res;
+  while (pos < lr.size() || !retry.empty()) {
+    jobs.clear();
+    if (!retry.empty()) {
+      jobs.swap(retry);
+    } else {
+      const size_t end = std::min(lr.size(), pos + batch);
+      for (size_t i = pos; i < end; ++i) {
+        const int64_t b = lr[i];
+        jobs.push_back(CompressJob{b, kest[H->level[b] * 8 + H->kind[b]]});
+      }
+      pos = end;
+    }
+    run_compress(H, pts, jobs, false, nullptr, res, st, workspace_budget());
+    for (size_t i = 0; i < jobs.size(); ++i) {
+      const int64_t b = jobs[i].block;
+      const CompressResult &r = res[i];
+      const int sh = H->d * (H->L - H->level[b]);
+      const int64_t m = H->leaf_start[(H->tgt[b] + 1) << sh] - H->leaf_start[H->tgt[b] << sh];
+      const int64_t n = H->leaf_start[(H->src[b] + 1) << sh] - H->leaf_start[H->src[b] << sh];
+      const int kfull = (int)std::min<int64_t>(std::min(m, n), KMAX);
+      if (!r.ok && r.k < kfull) {
+        retry.push_back(CompressJob{b, std::min(kfull, 2 * r.k)});
+        ++retries;
+        continue;
+      }
+      HH_REQUIRE(r.p >= 0, HH_EUNSUPPORTED, "block rank exceeds the sketch limit (512)");
+      HH_REQUIRE(std::isfinite(r.tot) && std::isfinite(r.nb2), HH_ENUMERIC, "non-finite kernel entry");
+      H->rank[b] = r.p;
+      H->kfinal[b] = r.k;
+      H->nb2[b] = r.nb2;
+      H->tot[b] = r.tot;
+      H->maxabs[b] = r.maxabs;
+      int &ke = kest[H->level[b] * 8 + H->kind[b]];
+      ke = std::max(ke, std::min(KMAX, ((r.p + 24 + 7) / 8) * 8));
+    }
+  }
+  H->info.n_retry = retries;
+}
+
+}  // namespace
+}  // namespace hh
+
+using namespace hh;
+
+extern "C" {
+
+const char *hh_last_error(void) { return g_err.c_str(); }
+int64_t hh_kernel_launches(void) { return g_launches.load(); }
+
+hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel, double eps, double eta,
+                   int32_t leaf_size, int32_t switch_level, uint32_t precision_set, void *cuda_stream,
+                   hh_handle *out) {
+  g_err.clear();
+  if (!points || !out) return fail(HH_EINVAL, "NULL pointer");
+  if (N < 1 || N > (int64_t)INT32_MAX) return fail(HH_EINVAL, "N must be in [1, 2^31)");
+  if (d < 1) return fail(HH_EINVAL, "d must be >= 1");
+  if (d > 3) return fail(HH_EUNSUPPORTED, "this build supports d <= 3");
+  if (!(eps > 0x1p-53 && eps < 1.0)) return fail(HH_EINVAL, "eps must be in (2^-53, 1)");
+  if (!(eta > 0.0) || !std::isfinite(eta)) return fail(HH_EINVAL, "eta must be > 0");
+  if (leaf_size < 1) return fail(HH_EINVAL, "leaf_size must be >= 1");
+  if (leaf_size > 256) return fail(HH_EUNSUPPORTED, "leaf_size > 256 not supported by this build");
+  if (!(precision_set & HH_P_FP64)) return fail(HH_EINVAL, "precision_set must contain HH_P_FP64");
+  if (precision_set & ~(0xFu | HH_LEDGER_ONLY)) return fail(HH_EINVAL, "unknown precision_set bits");
+  if (kernel.kind < 0 || kernel.kind > 4) return fail(HH_EINVAL, "unknown kernel kind");
+  if ((kernel.kind == HH_K_GAUSS || kernel.kind == HH_K_EXP) && !(kernel.scale > 0.0))
+    return fail(HH_EINVAL, "kernel scale must be > 0");
+  if (switch_level < HH_SWITCH_NONE) return fail(HH_EINVAL, "switch_level must be >= 0 or HH_SWITCH_NONE");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(HH_ECUDA, "no CUDA device");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  hh_matrix *H = nullptr;
+  try {
+    const auto t0 = std::chrono::steady_clock::now();
+    H = new hh_matrix();
+    H->N = N;
+    H->d = d;
+    H->kernel = kernel;
+    H->eps = eps;
+    H->eta = eta;
+    H->leaf_size = leaf_size;
+    H->s = switch_level;
+    H->pset = precision_set & 0xF;
+    H->ledger = (precision_set & HH_LEDGER_ONLY) != 0;
+    DBuf pts;
+    build_tree(H, points, st, pts);                                   // a1
+    HH_REQUIRE(switch_level == HH_SWITCH_NONE || switch_level <= H->L, HH_EINVAL, "switch_level > L");
+    build_partition(H);                                               // a2
+    const size_t nb = H->level.size();
+    const bool mixed = H->pset != HH_P_FP64;
+    H->storage.assign(nb, STORE_LR);
+    H->tag.assign(nb, TAG_FP64);
+    H->tot.assign(nb, 0.0);
+    std::vector<int64_t> lr, dn;
+    for (size_t b = 0; b < nb; ++b) {
+      const int k = H->kind[b];
+      if (k == KIND_DIAG || (k == KIND_LNBR && !mixed)) {
+        H->storage[b] = STORE_DENSE;
+        dn.push_back((int64_t)b);
+      } else {
+        lr.push_back((int64_t)b);
+      }
+    }
+    compress_all(H, pts.as<double>(), lr, st);                         // a3 (pass 1)
+    run_dense(H, pts.as<double>(), dn, false, st);                    // dense norms
+    for (size_t b = 0; b < nb; ++b)
+      HH_REQUIRE(std::isfinite(H->tot[b]), HH_ENUMERIC, "non-finite kernel entry");
+    assign_tags(H);                                                   // a4 + a5
+    compute_layout(H);                                                // a6 (offsets)
+    if (!H->ledger) {
+      for (int g = 0; g < 4; ++g) {
+        H->W[g].alloc(H->w_bytes[g]);
+        H->U[g].alloc(H->u_bytes[g]);
+        HH_CUDA(cudaMemsetAsync(H->U[g].p, 0, H->U[g].bytes, st));
+        HH_CUDA(cudaMemsetAsync(H->W[g].p, 0, H->W[g].bytes, st));
+      }
+      H->D.alloc(H->d_bytes);
+      HH_CUDA(cudaMemsetAsync(H->D.p, 0, H->D.bytes, st));
+      // pass 2: recompute (bitwise identical) and store rounded factors
+      DBuf d_uoff, d_ls, d_leaf_of;
+      h2d(d_uoff, H->u_leaf_off, st);
+      h2d(d_ls, H->leaf_start, st);
+      d_leaf_of.alloc(sizeof(int32_t) * N);
+      k_leaf_of<<<1184, 256, 0, st>>>(d_ls.as<int64_t>(), H->ncell, d_leaf_of.as<int32_t>());
+      HH_LAUNCHED();
+      Arenas ar{};
+      for (int g = 0; g < 4; ++g) {
+        ar.W[g] = H->W[g].as<uint8_t>();
+        ar.U[g] = H->U[g].as<uint8_t>();
+      }
+      ar.u_leaf_off = d_uoff.as<int64_t>();
+      ar.leaf_start = d_ls.as<int64_t>();
+      ar.leaf_of = d_leaf_of.as<int32_t>();
+      ar.ncell = H->ncell;
+      std::vector<CompressJob> jobs;
+      for (size_t b = 0; b < nb; ++b)
+        if (H->storage[b] == STORE_LR && H->rank[b] > 0) jobs.push_back(CompressJob{(int64_t)b, H->kfinal[b]});
+      std::vector<CompressResult> res;
+      run_compress(H, pts.as<double>(), jobs, true, &ar, res, st, workspace_budget());
+      int64_t mism = 0;
+      for (size_t i = 0; i < jobs.size(); ++i) mism += res[i].p != H->rank[jobs[i].block];
+      HH_REQUIRE(mism == 0, HH_ECUDA, "pass-2 recompression disagreed with pass 1 (non-deterministic kernel)");
+      // dense blocks (diagonal + dense neighbours) after tagging
+      std::vector<int64_t> dn2;
+      for (size_t b = 0; b < nb; ++b)
+        if (H->storage[b] == STORE_DENSE) dn2.push_back((int64_t)b);
+      run_dense(H, pts.as<double>(), dn2, true, st);
+      // matvec plan + workspace
+      std::vector<P1Item> items;
+      std::vector<P1Entry> entries;
+      std::vector<Combine> combines;
+      std::vector<P2Chunk> chunks;
+      std::vector<P2Leaf> leaves;
+      int64_t npart = 0;
+      build_plan(H, items, entries, combines, npart, chunks, leaves);
+      h2d(H->p1_items, items, st);
+      h2d(H->p1_entries, entries, st);
+      h2d(H->combines, combines, st);
+      h2d(H->p2_chunks, chunks, st);
+      h2d(H->p2_leaves, leaves, st);
+      H->n_p1_items = (int64_t)items.size();
+      H->n_combines = (int64_t)combines.size();
+      H->n_p2_leaves = (int64_t)leaves.size();
+      H->n_partials = npart;
+      H->partial.alloc(sizeof(double) * 16 * std::max<int64_t>(1, npart));
+      H->v.alloc(sizeof(double) * 16 * (size_t)(N + H->ztotal));
+      HH_CUDA(cudaStreamSynchronize(st));
+    }
+    // info
+    hh_info_t &I = H->info;
+    I.d = d;
+    I.L = H->L;
+    I.switch_level = switch_level;
+    I.kernel_kind = kernel.kind;
+    I.N = N;
+    I.eta = eta;
+    I.eps = eps;
+    I.kernel_scale = kernel.scale;
+    I.precision_set = H->pset;
+    I.ledger_only = H->ledger;
+    I.n_cells = H->ncell;
+    I.nblocks = (int64_t)nb;
+    I.total_rank = H->ztotal;
+    I.norm2 = H->norm2;
+    for (int g = 0; g < 4; ++g) {
+      I.w_bytes[g] = H->w_bytes[g];
+      I.u_bytes[g] = H->u_bytes[g];
+    }
+    I.d_bytes = H->d_bytes;
+    I.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = H;
+    return HH_OK;
+  } catch (const Error &e) {
+    delete H;
+    return fail(e.st, e.what());
+  } catch (const std::bad_alloc &) {
+    delete H;
+    return fail(HH_ENOMEM, "host allocation failed");
+  } catch (const std::exception &e) {
+    delete H;
+    return fail(HH_ECUDA, e.what());
+  }
+}
+
+hh_status hh_matvec(hh_handle H, const double *x, double *y, int32_t nrhs, void *cuda_stream) {
+  g_err.clear();
+  if (!H || !x || !y) return fail(HH_EINVAL, "NULL pointer");
+  if (nrhs < 1) return fail(HH_EINVAL, "nrhs must be >= 1");
+  if (H->ledger) return fail(HH_EINVAL, "ledger-only handle has no factors");
+  const char *xb = (const char *)x, *yb = (const char *)y;
+  const size_t bytes = sizeof(double) * (size_t)H->N * nrhs;
+  if (!(xb + bytes <= yb || yb + bytes <= xb)) return fail(HH_EINVAL, "x and y overlap");
+  try {
+    run_matvec(H, x, y, nrhs, (cudaStream_t)cuda_stream);
+    return HH_OK;
+  } catch (const Error &e) {
+    return fail(e.st, e.what());
+  }
+}
+
+hh_status hh_matvec_host(hh_handle H, const double *x_host, double *y_host, int32_t nrhs, void *cuda_stream) {
+  g_err.clear();
+  if (!H || !x_host || !y_host) return fail(HH_EINVAL, "NULL pointer");
+  if (nrhs < 1) return fail(HH_EINVAL, "nrhs must be >= 1");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  try {
+    DBuf dx, dy;
+    const size_t bytes = sizeof(double) * (size_t)H->N * nrhs;
+    dx.alloc(bytes);
+    dy.alloc(bytes);
+    HH_CUDA(cudaMemcpyAsync(dx.p, x_host, bytes, cudaMemcpyHostToDevice, st));
+    run_matvec(H, dx.as<double>(), dy.as<double>(), nrhs, st);
+    HH_CUDA(cudaMemcpyAsync(y_host, dy.p, bytes, cudaMemcpyDeviceToHost, st));
+    HH_CUDA(cudaStreamSynchronize(st));
+    return HH_OK;
+  } catch (const Error &e) {
+    return fail(e.st, e.what());
+  }
+}
+
+hh_status hh_info(hh_handle H, hh_info_t *info) {
+  if (!H || !info) return fail(HH_EINVAL, "NULL pointer");
+  *info = H->info;
+  return HH_OK;
+}
+
+hh_status hh_export(hh_handle H, hh_export_t *out) {
+  g_err.clear();
+  if (!H || !out) return fail(HH_EINVAL, "NULL pointer");
+  try {
+    out->info = H->info;
+    if (out->perm) HH_CUDA(cudaMemcpy(out->perm, H->d_perm.p, sizeof(int32_t) * H->N, cudaMemcpyDeviceToHost));
+    if (out->leaf_start) memcpy(out->leaf_start, H->leaf_start.data(), sizeof(int64_t) * H->leaf_start.size());
+    if (out->u_leaf_off && !H->u_leaf_off.empty())
+      memcpy(out->u_leaf_off, H->u_leaf_off.data(), sizeof(int64_t) * H->u_leaf_off.size());
+    if (out->d_leaf_off && !H->d_leaf_off.empty())
+      memcpy(out->d_leaf_off, H->d_leaf_off.data(), sizeof(int64_t) * H->d_leaf_off.size());
+    if (out->blocks) {
+      const size_t nb = H->level.size();
+      for (size_t b = 0; b < nb; ++b) {
+        hh_block_t &r = out->blocks[b];
+        r.tgt = H->tgt[b];
+        r.src = H->src[b];
+        r.zoff = H->zoff.empty() ? -1 : H->zoff[b];
+        r.w_off = H->w_off.empty() ? -1 : H->w_off[b];
+        r.ucol = H->ucol.empty() ? -1 : H->ucol[b];
+        r.d_off = H->d_off.empty() ? -1 : H->d_off[b];
+        r.nb2 = H->nb2.empty() ? 0 : H->nb2[b];
+        r.tot = H->tot[b];
+        r.maxabs = H->maxabs.empty() ? 0 : H->maxabs[b];
+        r.rank = H->rank[b];
+        r.level = H->level[b];
+        r.kind = H->kind[b];
+        r.tag = H->tag[b];
+        r.storage = H->storage[b];
+      }
+    }
+    if (out->arena_dst && out->arena_len > 0) {
+      if (H->ledger) return fail(HH_EINVAL, "ledger-only handle has no arenas");
+      const DBuf *src = nullptr;
+      if (out->arena >= 0 && out->arena < 4) src = &H->W[out->arena];
+      else if (out->arena >= 4 && out->arena < 8) src = &H->U[out->arena - 4];
+      else if (out->arena == 8) src = &H->D;
+      if (!src) return fail(HH_EINVAL, "arena must be 0..8");
+      const int64_t size = out->arena < 4 ? H->w_bytes[out->arena]
+                           : out->arena < 8 ? H->u_bytes[out->arena - 4] : H->d_bytes;
+      if (out->arena_off < 0 || out->arena_off + out->arena_len > size) return fail(HH_EINVAL, "arena window out of range");
+      HH_CUDA(cudaMemcpy(out->arena_dst, (const char *)src->p + out->arena_off, out->arena_len, cudaMemcpyDeviceToHost));
+    }
+    return HH_OK;
+  } catch (const Error &e) {
+    return fail(e.st, e.what());
+  }
+}
+
+hh_status hh_free(hh_handle H) {
+  delete H;
+  return HH_OK;
+}
+
+/* Test hook: apply the device storage-rounding routine of `tag` (1..3) to host values and
+ * return the bit patterns (checked against the oracle's definition-based rounding). */
+hh_status hh_selftest_round(const double *host_in, int64_t n, int32_t tag, uint32_t *host_bits) {
+  g_err.clear();
+  if (!host_in || !host_bits || n < 0 || tag < 1 || tag > 3) return fail(HH_EINVAL, "bad argument");
+  try {
+    DBuf a, b;
+    a.alloc(sizeof(double) * n);
+    b.alloc(sizeof(uint32_t) * n);
+    HH_CUDA(cudaMemcpy(a.p, host_in, sizeof(double) * n, cudaMemcpyHostToDevice));
+    k_round<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256>>>(a.as<double>(), n, tag, b.as<uint32_t>());
+    HH_LAUNCHED();
+    HH_CUDA(cudaMemcpy(host_bits, b.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+    return HH_OK;
+  } catch (const Error &e) {
+    return fail(e.st, e.what());
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,44 @@
+// build.h — declarations shared by the build-pipeline translation units.
+#pragma once
+#include <vector>
+
+#include "handle.h"
+
+namespace hh {
+
+struct CompressJob {
+  int64_t block;  // index into the handle's block table
+  int32_t k;      // sketch width
+};
+
+struct CompressResult {
+  int32_t p, k;
+  double nb2, tot, R, maxabs;
+  int32_t ok;
+};
+
+// Pass-2 output placement (device pointers).
+struct Arenas {
+  uint8_t *W[4];
+  uint8_t *U[4];
+  const int64_t *u_leaf_off;  // [4][ncell+1]
+  const int64_t *leaf_start;  // [ncell+1]
+  const int32_t *leaf_of;     // [N] tree position -> leaf cell
+  int64_t ncell;
+};
+
+KernelFn make_kernel_fn(const hh_kernel &kk);
+void build_tree(hh_matrix *H, const double *P, cudaStream_t st, DBuf &pts_tree);
+void build_partition(hh_matrix *H);
+void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob> &jobs, bool write,
+                  const Arenas *ar, std::vector<CompressResult> &res, cudaStream_t st, size_t ws_budget);
+void run_dense(hh_matrix *H, const double *pts, const std::vector<int64_t> &blocks, bool fill, cudaStream_t st);
+void assign_tags(hh_matrix *H);
+void compute_layout(hh_matrix *H);
+void cluster_range(const hh_matrix *H, int l, int64_t m, int64_t &a, int64_t &n);
+void build_plan(hh_matrix *H, std::vector<P1Item> &items, std::vector<P1Entry> &entries,
+                std::vector<Combine> &combines, int64_t &npartial, std::vector<P2Chunk> &chunks,
+                std::vector<P2Leaf> &leaves);
+void run_matvec(hh_matrix *H, const double *x, double *y, int nrhs, cudaStream_t st);
+
+}  // namespace hh

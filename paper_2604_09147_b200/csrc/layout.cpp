@@ -1,0 +1,353 @@
+// layout.cpp — §8(a) rows a4–a6 (host side): global norm, precision tags, packing function,
+// and the matvec work plan.
+//
+//   a4  ||H~||^2 = sum_b nb2_b over low-rank blocks + sum ||H_b||^2 over dense blocks; for
+//       pure H_s the leaf neighbours enter with their direct norm (Alg. 4).
+//   a5  Eq. 4.4 / Alg. 2 in squared exact form (G15):
+//           u^2 2^{d l} nb2_b <= eps^2 ||H~||^2,  largest such u in the precision set;
+//       none -> fp64 (fallback); range guard promotes when a factor entry would overflow;
+//       pure H_s mixed: leaf neighbour low-rank iff p(|I|+|J|) bits < |I||J| 64.
+//   a6  packing function — the C++ twin of the oracle's pack.py, written
+//       independently; check (1c) compares them bit for bit.
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <vector>
+
+#include "build.h"
+
+namespace hh {
+
+static const double kU[4] = {0x1p-53, 0x1p-24, 0x1p-11, 0x1p-8};
+static const double kOverflow[4] = {INFINITY, 0x1.ffffffp127, 65520.0, 0x1.fep127};  // |x| >= this rounds to inf
+static const uint32_t kBit[4] = {HH_P_FP64, HH_P_FP32, HH_P_FP16, HH_P_BF16};
+
+void cluster_range(const hh_matrix *H, int l, int64_t m, int64_t &a, int64_t &n) {
+  const int sh = H->d * (H->L - l);
+  a = H->leaf_start[m << sh];
+  n = H->leaf_start[(m + 1) << sh] - a;
+}
+
+void assign_tags(hh_matrix *H) {
+  const size_t nb = H->level.size();
+  const bool mixed = (H->pset & 0xF) != HH_P_FP64;
+  // a4: global norm in canonical order
+  double norm2 = 0.0;
+  for (size_t b = 0; b < nb; ++b) {
+    const int k = H->kind[b];
+    norm2 += (k == KIND_DIAG || k == KIND_LNBR) ? H->tot[b] : H->nb2[b];
+  }
+  H->norm2 = norm2;
+  const double rhs = (H->eps * H->eps) * norm2;
+  int64_t fb = 0, pr = 0;
+  for (size_t b = 0; b < nb; ++b) {
+    if (H->storage[b] != STORE_LR) continue;
+    const int l = H->level[b];
+    int tag = TAG_FP64;
+    bool found = false;
+    const int order[4] = {TAG_BF16, TAG_FP16, TAG_FP32, TAG_FP64};
+    for (int t : order) {
+      if (!(H->pset & kBit[t])) continue;
+      const double u = kU[t];
+      if ((u * u) * std::ldexp(1.0, H->d * l) * H->nb2[b] <= rhs) {
+        tag = t;
+        found = true;
+        break;
+      }
+    }
+    fb += !found;
+    // range guard: promote while the largest factor entry would overflow the format
+    while (tag != TAG_FP64 && H->maxabs[b] >= kOverflow[tag]) {
+      int nt = tag == TAG_BF16 ? TAG_FP16 : tag == TAG_FP16 ? TAG_FP32 : TAG_FP64;
+      while (nt != TAG_FP64 && !(H->pset & kBit[nt])) nt = nt == TAG_FP16 ? TAG_FP32 : TAG_FP64;
+      tag = nt;
+      ++pr;
+    }
+    H->tag[b] = (uint8_t)tag;
+    if (H->kind[b] == KIND_LNBR && mixed) {
+      int64_t i0, m, j0, n;
+      cluster_range(H, l, H->tgt[b], i0, m);
+      cluster_range(H, l, H->src[b], j0, n);
+      const int bits = 8 * tag_bytes(tag);
+      if (!((int64_t)H->rank[b] * (m + n) * bits < m * n * 64)) {
+        H->storage[b] = STORE_DENSE;
+        H->rank[b] = 0;
+        H->tag[b] = TAG_FP64;
+      }
+    }
+  }
+  H->info.n_fallback = fb;
+  H->info.n_promoted = pr;
+}
+
+// a6: packing function.  Fills zoff, w_off, ucol, u_leaf_off, d_off, d_leaf_off and sizes.
+void compute_layout(hh_matrix *H) {
+  const size_t nb = H->level.size();
+  const int d = H->d, L = H->L;
+  const int64_t ncell = H->ncell;
+  H->zoff.assign(nb, -1);
+  H->w_off.assign(nb, -1);
+  H->ucol.assign(nb, -1);
+  H->d_off.assign(nb, -1);
+  std::vector<int64_t> I0(nb), M(nb), J0(nb), Nn(nb);
+  for (size_t b = 0; b < nb; ++b) {
+    cluster_range(H, H->level[b], H->tgt[b], I0[b], M[b]);
+    cluster_range(H, H->level[b], H->src[b], J0[b], Nn[b]);
+  }
+  auto is_lr = [&](size_t b) { return H->storage[b] == STORE_LR; };
+  // z: (level, tgt, tag, src); canonical order is (level, tgt, src): stable-sort by tag
+  // inside each (level, tgt) run
+  {
+    int64_t z = 0;
+    size_t b = 0;
+    while (b < nb) {
+      size_t e = b;
+      while (e < nb && H->level[e] == H->level[b] && H->tgt[e] == H->tgt[b]) ++e;
+      for (int t = 0; t < 4; ++t)
+        for (size_t i = b; i < e; ++i)
+          if (is_lr(i) && H->tag[i] == t) {
+            H->zoff[i] = z;
+            z += H->rank[i];
+          }
+      b = e;
+    }
+    H->ztotal = z;
+  }
+  // W[g]: tag-g low-rank blocks with p > 0 in (level, src, tgt) order, 16-B aligned
+  {
+    std::vector<size_t> idx;
+    for (size_t b = 0; b < nb; ++b)
+      if (is_lr(b) && H->rank[b] > 0) idx.push_back(b);
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t c) {
+      if (H->level[a] != H->level[c]) return H->level[a] < H->level[c];
+      if (H->src[a] != H->src[c]) return H->src[a] < H->src[c];
+      return H->tgt[a] < H->tgt[c];
+    });
+    int64_t off[4] = {0, 0, 0, 0};
+    for (size_t b : idx) {
+      const int g = H->tag[b];
+      H->w_off[b] = off[g];
+      off[g] += align_up(Nn[b] * H->rank[b] * tag_bytes(g));
+    }
+    for (int g = 0; g < 4; ++g) H->w_bytes[g] = off[g];
+  }
+  // U[g]: per-leaf streams.  Column base of block b = columns of coarser levels of its
+  // target's ancestors + prefix inside its (level, tgt, tag) group.
+  {
+    // group totals per (level, tgt, tag)
+    std::vector<std::vector<int64_t>> gtot(L + 1);
+    for (int l = 0; l <= L; ++l) gtot[l].assign((size_t)4 << (d * l), 0);
+    for (size_t b = 0; b < nb; ++b)
+      if (is_lr(b) && H->rank[b] > 0) gtot[H->level[b]][(size_t)H->tgt[b] * 4 + H->tag[b]] += H->rank[b];
+    // coarser-level column base per (level, tgt, tag): base[l][t] = sum_{l' < l} gtot[l'][anc(t)]
+    std::vector<std::vector<int64_t>> base(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      base[l].assign((size_t)4 << (d * l), 0);
+      if (l > 0)
+        for (int64_t t = 0; t < (1ll << (d * l)); ++t)
+          for (int g = 0; g < 4; ++g)
+            base[l][t * 4 + g] = base[l - 1][(t >> d) * 4 + g] + gtot[l - 1][(t >> d) * 4 + g];
+    }
+    std::vector<int64_t> run(4, 0);
+    size_t b = 0;
+    while (b < nb) {
+      size_t e = b;
+      while (e < nb && H->level[e] == H->level[b] && H->tgt[e] == H->tgt[b]) ++e;
+      int64_t within[4] = {0, 0, 0, 0};
+      for (size_t i = b; i < e; ++i)
+        if (is_lr(i) && H->rank[i] > 0) {
+          const int g = H->tag[i];
+          H->ucol[i] = base[H->level[i]][(size_t)H->tgt[i] * 4 + g] + within[g];
+          within[g] += H->rank[i];
+        }
+      b = e;
+    }
+    H->u_leaf_off.assign((size_t)4 * (ncell + 1), 0);
+    for (int g = 0; g < 4; ++g) {
+      int64_t off = 0;
+      for (int64_t R = 0; R < ncell; ++R) {
+        H->u_leaf_off[(size_t)g * (ncell + 1) + R] = off;
+        const int64_t nr = H->leaf_start[R + 1] - H->leaf_start[R];
+        const int64_t cols = base[L][(size_t)R * 4 + g] + gtot[L][(size_t)R * 4 + g];
+        off += align_up(nr * cols * tag_bytes(g));
+      }
+      H->u_leaf_off[(size_t)g * (ncell + 1) + ncell] = off;
+      H->u_bytes[g] = off;
+    }
+  }
+  // dense arena: per target leaf, src order, 16-B aligned leaf groups
+  {
+    H->d_leaf_off.assign(ncell + 1, 0);
+    std::vector<int64_t> per(ncell, 0);
+    for (size_t b = 0; b < nb; ++b)
+      if (H->storage[b] == STORE_DENSE) per[H->tgt[b]] += M[b] * Nn[b] * 8;
+    int64_t off = 0;
+    for (int64_t R = 0; R < ncell; ++R) {
+      H->d_leaf_off[R] = off;
+      off += align_up(per[R]);
+    }
+    H->d_leaf_off[ncell] = off;
+    H->d_bytes = off;
+    std::vector<int64_t> cur(H->d_leaf_off.begin(), H->d_leaf_off.end() - 1);
+    for (size_t b = 0; b < nb; ++b)  // canonical order = (tgt, src) inside level L
+      if (H->storage[b] == STORE_DENSE) {
+        H->d_off[b] = cur[H->tgt[b]];
+        cur[H->tgt[b]] += M[b] * Nn[b] * 8;
+      }
+  }
+  // ledger
+  int64_t tagged[5] = {0, 0, 0, 0, 0};
+  int64_t nlr = 0, nd = 0;
+  for (size_t b = 0; b < nb; ++b) {
+    if (H->storage[b] == STORE_DENSE) {
+      tagged[4] += M[b] * Nn[b] * 8;
+      ++nd;
+    } else {
+      tagged[H->tag[b]] += (int64_t)H->rank[b] * (M[b] + Nn[b]) * tag_bytes(H->tag[b]);
+      ++nlr;
+    }
+  }
+  int64_t tot = 0, pad = H->d_bytes;
+  for (int i = 0; i < 5; ++i) {
+    H->info.stored_bytes_tag[i] = tagged[i];
+    tot += tagged[i];
+  }
+  for (int g = 0; g < 4; ++g) pad += H->w_bytes[g] + H->u_bytes[g];
+  H->info.stored_bytes = tot;
+  H->info.padded_bytes = pad;
+  H->info.n_lowrank = nlr;
+  H->info.n_dense = nd;
+}
+
+// ----------------------------------------------------------------- matvec work plan
+constexpr int64_t STAGE_BYTES = 16384;
+
+void build_plan(hh_matrix *H, std::vector<P1Item> &items, std::vector<P1Entry> &entries,
+                std::vector<Combine> &combines, int64_t &npartial, std::vector<P2Chunk> &chunks,
+                std::vector<P2Leaf> &leaves) {
+  const size_t nb = H->level.size();
+  const int d = H->d, L = H->L;
+  const int64_t N = H->N;
+  items.clear();
+  entries.clear();
+  combines.clear();
+  chunks.clear();
+  leaves.clear();
+  npartial = 0;
+  // ---- phase 1: W arenas in storage order
+  std::vector<size_t> idx;
+  for (size_t b = 0; b < nb; ++b)
+    if (H->storage[b] == STORE_LR && H->rank[b] > 0) idx.push_back(b);
+  std::sort(idx.begin(), idx.end(), [&](size_t a, size_t c) {
+    if (H->tag[a] != H->tag[c]) return H->tag[a] < H->tag[c];
+    return H->w_off[a] < H->w_off[c];
+  });
+  P1Item cur{};
+  bool open = false;
+  auto flush = [&]() {
+    if (open && cur.e1 > cur.e0) items.push_back(cur);
+    open = false;
+  };
+  for (size_t b : idx) {
+    const int g = H->tag[b];
+    const int w = tag_bytes(g);
+    int64_t j0, n, i0, m;
+    cluster_range(H, H->level[b], H->src[b], j0, n);
+    cluster_range(H, H->level[b], H->tgt[b], i0, m);
+    const int p = H->rank[b];
+    const int64_t bytes = n * p * w, pbytes = align_up(bytes);
+    if (open && (cur.tag != g || (int64_t)cur.nbytes + pbytes > STAGE_BYTES)) flush();
+    if (pbytes <= STAGE_BYTES) {
+      if (!open) {
+        cur = P1Item{H->w_off[b], 0, (uint16_t)g, 0, (uint32_t)entries.size(), (uint32_t)entries.size()};
+        open = true;
+      }
+      entries.push_back(P1Entry{(uint32_t)(H->w_off[b] - cur.src), (uint32_t)n, (uint32_t)p, 0, j0, H->zoff[b]});
+      cur.nbytes += (uint32_t)pbytes;
+      cur.e1 = (uint32_t)entries.size();
+      continue;
+    }
+    flush();
+    const int64_t cb = n * w;
+    if (cb + 32 <= STAGE_BYTES) {  // runs of whole columns
+      const int64_t cpi = (STAGE_BYTES - 32) / cb;
+      for (int64_t c0 = 0; c0 < p; c0 += cpi) {
+        const int64_t c1 = std::min<int64_t>(p, c0 + cpi);
+        const int64_t s = H->w_off[b] + c0 * cb, e = H->w_off[b] + c1 * cb;
+        const int64_t sa = s / ALIGN * ALIGN, ea = align_up(e);
+        items.push_back(P1Item{sa, (uint32_t)(ea - sa), (uint16_t)g, 0, (uint32_t)entries.size(), (uint32_t)entries.size() + 1});
+        entries.push_back(P1Entry{(uint32_t)(s - sa), (uint32_t)n, (uint32_t)(c1 - c0), 0, j0, H->zoff[b] + c0});
+      }
+    } else {  // a column longer than a stage: row pieces + fixed-order combine
+      const int64_t rpi = ((STAGE_BYTES - 32) / w) / 32 * 32;
+      for (int64_t c = 0; c < p; ++c) {
+        Combine cm{H->zoff[b] + c, npartial, npartial};
+        for (int64_t r0 = 0; r0 < n; r0 += rpi) {
+          const int64_t r1 = std::min(n, r0 + rpi);
+          const int64_t s = H->w_off[b] + (c * n + r0) * w, e = H->w_off[b] + (c * n + r1) * w;
+          const int64_t sa = s / ALIGN * ALIGN, ea = align_up(e);
+          items.push_back(P1Item{sa, (uint32_t)(ea - sa), (uint16_t)g, 0, (uint32_t)entries.size(), (uint32_t)entries.size() + 1});
+          entries.push_back(P1Entry{(uint32_t)(s - sa), (uint32_t)(r1 - r0), 1, 0, j0 + r0, ~npartial});
+          ++npartial;
+        }
+        cm.s1 = npartial;
+        combines.push_back(cm);
+      }
+    }
+  }
+  flush();
+  // ---- phase 2: per leaf, per tag, per level groups; then dense blocks
+  // group (level, tgt, tag) -> (zbeg, P)
+  std::vector<std::vector<int64_t>> gz(L + 1), gp(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    gz[l].assign((size_t)4 << (d * l), -1);
+    gp[l].assign((size_t)4 << (d * l), 0);
+  }
+  for (size_t b = 0; b < nb; ++b)
+    if (H->storage[b] == STORE_LR && H->rank[b] > 0) {
+      const size_t key = (size_t)H->tgt[b] * 4 + H->tag[b];
+      if (gz[H->level[b]][key] < 0) gz[H->level[b]][key] = H->zoff[b];
+      gp[H->level[b]][key] += H->rank[b];
+    }
+  // dense blocks by target leaf
+  std::vector<std::vector<size_t>> dense(H->ncell);
+  for (size_t b = 0; b < nb; ++b)
+    if (H->storage[b] == STORE_DENSE) dense[H->tgt[b]].push_back(b);
+  auto add_cols = [&](int64_t base, int64_t nr, int64_t ncols, int w, int tag, int isdense, int64_t vbeg) {
+    const int64_t cb = nr * w;
+    const int64_t cpc = std::max<int64_t>(1, (STAGE_BYTES - 32) / cb);
+    for (int64_t c0 = 0; c0 < ncols; c0 += cpc) {
+      const int64_t c1 = std::min(ncols, c0 + cpc);
+      const int64_t s = base + c0 * cb, e = base + c1 * cb;
+      const int64_t sa = s / ALIGN * ALIGN, ea = align_up(e);
+      chunks.push_back(P2Chunk{sa, (uint32_t)(ea - sa), (uint32_t)(s - sa), (uint32_t)(c1 - c0), (uint16_t)tag,
+                               (uint16_t)isdense, vbeg + c0});
+    }
+  };
+  for (int64_t R = 0; R < H->ncell; ++R) {
+    const int64_t r0 = H->leaf_start[R], nr = H->leaf_start[R + 1] - r0;
+    if (nr == 0) continue;
+    P2Leaf lf{r0, (int32_t)nr, 0, (int64_t)chunks.size(), 0};
+    for (const size_t b : dense[R]) {
+      int64_t j0, n;
+      cluster_range(H, H->level[b], H->src[b], j0, n);
+      add_cols(H->d_off[b], nr, n, 8, TAG_FP64, 1, j0);
+    }
+    for (int g = 0; g < 4; ++g) {
+      const int w = tag_bytes(g);
+      int64_t col = 0;
+      const int64_t base = H->u_leaf_off[(size_t)g * (H->ncell + 1) + R];
+      for (int l = 0; l <= L; ++l) {
+        const size_t key = (size_t)(R >> (d * (L - l))) * 4 + g;
+        const int64_t P = gp[l][key];
+        if (P == 0) continue;
+        add_cols(base + col * nr * w, nr, P, w, g, 0, N + gz[l][key]);
+        col += P;
+      }
+    }
+    lf.c1 = (int64_t)chunks.size();
+    leaves.push_back(lf);
+  }
+}
+
+}  // namespace hh

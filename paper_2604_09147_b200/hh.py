@@ -1,0 +1,212 @@
+"""Thin ctypes binding of libhh (include/hh.h) — argument marshalling only.
+
+Every step of the build and of the matvec runs inside libhh.so's CUDA kernels; this module
+only converts torch tensors / numpy arrays to pointers and back.  There is no CPU fallback:
+if the shared library is missing, importing the binding raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhh.so")
+
+HH_OK, HH_EINVAL, HH_ENOMEM, HH_ECUDA, HH_ENUMERIC, HH_EDEPTH, HH_EUNSUPPORTED = range(7)
+K_LOG, K_INV_R, K_INV_R2, K_GAUSS, K_EXP = range(5)
+P_FP64, P_FP32, P_FP16, P_BF16 = 1, 2, 4, 8
+P_MIXED = 15
+LEDGER_ONLY = 1 << 16
+SWITCH_NONE = -1
+ARENA_W, ARENA_U, ARENA_D = 0, 4, 8
+
+
+class HHError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"hh status {status}: {msg}")
+        self.status = status
+
+
+class hh_kernel(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("scale", C.c_double)]
+
+
+class hh_info_t(C.Structure):
+    _fields_ = [
+        ("d", C.c_int32), ("L", C.c_int32), ("switch_level", C.c_int32), ("kernel_kind", C.c_int32),
+        ("N", C.c_int64), ("eta", C.c_double), ("eps", C.c_double), ("kernel_scale", C.c_double),
+        ("precision_set", C.c_uint32), ("ledger_only", C.c_int32),
+        ("n_cells", C.c_int64), ("nblocks", C.c_int64), ("n_lowrank", C.c_int64), ("n_dense", C.c_int64),
+        ("total_rank", C.c_int64), ("norm2", C.c_double),
+        ("w_bytes", C.c_int64 * 4), ("u_bytes", C.c_int64 * 4), ("d_bytes", C.c_int64),
+        ("stored_bytes", C.c_int64), ("stored_bytes_tag", C.c_int64 * 5), ("padded_bytes", C.c_int64),
+        ("c_far", C.c_int32), ("c_nbr", C.c_int32), ("c_sib", C.c_int32),
+        ("n_fallback", C.c_int64), ("n_promoted", C.c_int64), ("n_coincident", C.c_int64), ("n_retry", C.c_int64),
+        ("build_seconds", C.c_double),
+    ]
+
+    def as_dict(self):
+        out = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            out[name] = list(v) if hasattr(v, "__len__") else v
+        return out
+
+
+BLOCK_DTYPE = np.dtype([
+    ("tgt", "<i8"), ("src", "<i8"), ("zoff", "<i8"), ("w_off", "<i8"), ("ucol", "<i8"), ("d_off", "<i8"),
+    ("nb2", "<f8"), ("tot", "<f8"), ("maxabs", "<f8"), ("rank", "<i4"),
+    ("level", "u1"), ("kind", "u1"), ("tag", "u1"), ("storage", "u1"),
+])
+assert BLOCK_DTYPE.itemsize == 80
+
+
+class hh_export_t(C.Structure):
+    _fields_ = [
+        ("info", hh_info_t), ("perm", C.c_void_p), ("leaf_start", C.c_void_p), ("blocks", C.c_void_p),
+        ("u_leaf_off", C.c_void_p), ("d_leaf_off", C.c_void_p),
+        ("arena", C.c_int32), ("arena_off", C.c_int64), ("arena_len", C.c_int64), ("arena_dst", C.c_void_p),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2604_09147_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    lib.hh_build.argtypes = [C.c_void_p, C.c_int64, C.c_int32, hh_kernel, C.c_double, C.c_double, C.c_int32,
+                             C.c_int32, C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.hh_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+    lib.hh_matvec_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+    lib.hh_info.argtypes = [C.c_void_p, C.POINTER(hh_info_t)]
+    lib.hh_export.argtypes = [C.c_void_p, C.POINTER(hh_export_t)]
+    lib.hh_free.argtypes = [C.c_void_p]
+    lib.hh_last_error.restype = C.c_char_p
+    lib.hh_kernel_launches.restype = C.c_int64
+    lib.hh_selftest_round.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]
+    for f in ("hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_selftest_round"):
+        getattr(lib, f).restype = C.c_int
+    return lib
+
+
+lib = _load()
+EXPORTED = ["hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_last_error",
+            "hh_kernel_launches", "hh_selftest_round"]
+
+
+def _check(st):
+    if st != HH_OK:
+        raise HHError(st, lib.hh_last_error().decode())
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
+
+
+class Handle:
+    """Owns an hh_handle; freed with hh_free on close()/garbage collection."""
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def close(self):
+        if self.ptr:
+            lib.hh_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def hh_build(points, kernel: int, scale: float, eps: float, eta: float, leaf_size: int, switch_level: int,
+             precision_set: int, stream=None) -> Handle:
+    """points: torch CUDA float64 tensor (N, d), contiguous."""
+    assert points.is_cuda and points.dtype.is_floating_point and points.element_size() == 8
+    points = points.contiguous()
+    out = C.c_void_p()
+    N, d = points.shape
+    _check(lib.hh_build(C.c_void_p(points.data_ptr()), N, d, hh_kernel(kernel, scale), eps, eta, leaf_size,
+                        switch_level, precision_set, _stream_ptr(stream), C.byref(out)))
+    return Handle(out.value)
+
+
+def hh_matvec(H: Handle, x, y, nrhs: int | None = None, stream=None):
+    """x, y: torch CUDA float64 tensors of shape (N,) or (N, nrhs) — column-major storage
+    (pass x.T.contiguous().T or a Fortran-ordered view); y is overwritten."""
+    nrhs = nrhs or (1 if x.dim() == 1 else x.shape[1])
+    assert x.is_cuda and y.is_cuda
+    if x.dim() == 2:
+        assert x.stride(0) == 1 and y.stride(0) == 1, "x/y must be column-major (N, nrhs)"
+    _check(lib.hh_matvec(H.ptr, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), nrhs, _stream_ptr(stream)))
+
+
+def hh_matvec_host(H: Handle, x: np.ndarray, y: np.ndarray | None = None, stream=None) -> np.ndarray:
+    """Host float64 arrays (N,) or (N, nrhs) Fortran order; host<->device copies inside."""
+    x = np.asfortranarray(x, dtype=np.float64)
+    nrhs = 1 if x.ndim == 1 else x.shape[1]
+    if y is None:
+        y = np.empty_like(x, order="F")
+    _check(lib.hh_matvec_host(H.ptr, x.ctypes.data, y.ctypes.data, nrhs, _stream_ptr(stream)))
+    return y
+
+
+def hh_info(H: Handle) -> dict:
+    info = hh_info_t()
+    _check(lib.hh_info(H.ptr, C.byref(info)))
+    return info.as_dict()
+
+
+def hh_export(H: Handle, tables: bool = True, arenas: bool = True) -> dict:
+    """Export tables and (optionally) every arena to numpy (host memory)."""
+    info = hh_info(H)
+    out = {"info": info}
+    e = hh_export_t()
+    if tables:
+        perm = np.empty(info["N"], np.int32)
+        ls = np.empty(info["n_cells"] + 1, np.int64)
+        blocks = np.empty(info["nblocks"], BLOCK_DTYPE)
+        uoff = np.empty(4 * (info["n_cells"] + 1), np.int64)
+        doff = np.empty(info["n_cells"] + 1, np.int64)
+        e.perm, e.leaf_start, e.blocks = perm.ctypes.data, ls.ctypes.data, blocks.ctypes.data
+        e.u_leaf_off, e.d_leaf_off = uoff.ctypes.data, doff.ctypes.data
+        _check(lib.hh_export(H.ptr, C.byref(e)))
+        out.update(perm=perm, leaf_start=ls, blocks=blocks, u_leaf_off=uoff.reshape(4, -1), d_leaf_off=doff)
+    if arenas and not info["ledger_only"]:
+        for g in range(4):
+            out[("W", g)] = export_arena(H, ARENA_W + g, 0, info["w_bytes"][g])
+            out[("U", g)] = export_arena(H, ARENA_U + g, 0, info["u_bytes"][g])
+        out["D"] = export_arena(H, ARENA_D, 0, info["d_bytes"])
+    return out
+
+
+def export_arena(H: Handle, arena: int, off: int, length: int) -> np.ndarray:
+    buf = np.zeros(length, np.uint8)
+    if length == 0:
+        return buf
+    e = hh_export_t()
+    e.arena, e.arena_off, e.arena_len, e.arena_dst = arena, off, length, buf.ctypes.data
+    _check(lib.hh_export(H.ptr, C.byref(e)))
+    return buf
+
+
+def hh_free(H: Handle):
+    H.close()
+
+
+def kernel_launches() -> int:
+    return int(lib.hh_kernel_launches())
+
+
+def selftest_round(x: np.ndarray, tag: int) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty(x.size, np.uint32)
+    _check(lib.hh_selftest_round(x.ctypes.data, x.size, tag, out.ctypes.data))
+    return out

@@ -1,0 +1,115 @@
+"""Helpers for GPU-vs-oracle parity (used by tests/test_gpu_*.py, __graft_entry__.smoke and
+bench.py's reference leg).  Test infrastructure: may import oracle/."""
+from __future__ import annotations
+
+import numpy as np
+
+import workloads as W
+from oracle import formats as F
+from oracle import hmatrix as HM
+from oracle import matvec as MV
+from oracle import pack as PK
+from oracle import tree as T
+
+
+def gpu_build(P: np.ndarray, cfg: dict, pset=None, s=None):
+    import torch
+    from paper_2604_09147_b200 import hh
+    Pd = torch.from_numpy(np.ascontiguousarray(P)).cuda()
+    H = hh.hh_build(Pd, cfg["kernel"], cfg["scale"], cfg["eps"], cfg["eta"], cfg["leaf"],
+                    cfg["s"] if s is None else s, cfg["pset"] if pset is None else pset)
+    torch.cuda.synchronize()
+    return H
+
+
+def export(H, arenas=True):
+    from paper_2604_09147_b200 import hh
+    return hh.hh_export(H, tables=True, arenas=arenas)
+
+
+def check_partition(ex, Ho):
+    """Check (1a): perm, leaf offsets and the block table (level, kind, tgt, src) bit-exact."""
+    np.testing.assert_array_equal(ex["perm"].astype(np.int64), Ho.tree.perm)
+    np.testing.assert_array_equal(ex["leaf_start"], Ho.tree.leaf_start)
+    B = ex["blocks"]
+    assert B.size == len(Ho.part)
+    for name, ref in (("level", Ho.part.level), ("kind", Ho.part.kind), ("tgt", Ho.part.tgt), ("src", Ho.part.src)):
+        np.testing.assert_array_equal(B[name].astype(np.int64), ref, err_msg=name)
+
+
+def oracle_partition(P, cfg, s=None):
+    from oracle import partition as PT
+    tr = T.build_tree(P, cfg["leaf"])
+    return tr, PT.build_partition(tr, cfg["eta"], cfg["s"] if s is None else s)
+
+
+def check_packing(ex):
+    """Check (1c): the oracle's packing function on the GPU's (rank, tag, storage) reproduces
+    every exported offset bit for bit."""
+    B = ex["blocks"]
+    d, L = ex["info"]["d"], ex["info"]["L"]
+    lay = PK.pack(ex["leaf_start"], d, L, B["level"], B["tgt"], B["src"], B["rank"], B["tag"], B["storage"])
+    lr = B["storage"] == 0
+    np.testing.assert_array_equal(lay["zoff"][lr], B["zoff"][lr], err_msg="zoff")
+    has = lr & (B["rank"] > 0)
+    np.testing.assert_array_equal(lay["w_off"][has], B["w_off"][has], err_msg="w_off")
+    np.testing.assert_array_equal(lay["ucol"][has], B["ucol"][has], err_msg="ucol")
+    dn = ~lr
+    np.testing.assert_array_equal(lay["d_off"][dn], B["d_off"][dn], err_msg="d_off")
+    np.testing.assert_array_equal(lay["u_leaf_off"], ex["u_leaf_off"], err_msg="u_leaf_off")
+    np.testing.assert_array_equal(lay["d_leaf_off"], ex["d_leaf_off"], err_msg="d_leaf_off")
+    info = ex["info"]
+    np.testing.assert_array_equal(lay["w_bytes"], np.array(info["w_bytes"]), err_msg="w_bytes")
+    assert lay["ztotal"] == info["total_rank"]
+    return lay
+
+
+def exported_blocks(ex, lay):
+    """Decode every block of the export with the ORACLE's packing function -> Alg. 3 input."""
+    B = ex["blocks"]
+    d, L = ex["info"]["d"], ex["info"]["L"]
+    for b in range(B.size):
+        kind, payload = PK.unpack_block(lay, b, ex["leaf_start"], d, L, B["level"], B["tgt"], B["rank"],
+                                        B["tag"], B["storage"], ex)
+        i0, j0 = int(lay["i0"][b]), int(lay["j0"][b])
+        yield i0, i0 + int(lay["m"][b]), j0, j0 + int(lay["n"][b]), kind, payload
+
+
+def oracle_matvec_on_export(ex, lay, x):
+    return MV.matvec_blocks(ex["info"]["N"], ex["perm"].astype(np.int64), exported_blocks(ex, lay), x)
+
+
+def rank_tag_parity(ex, Ho, rank_margin=1e-6, tag_margin=1e-9):
+    """Check (1b): rank and tag per block equal to the oracle's truncated-SVD rank and Eq. 4.4
+    tag.  A difference is tolerated only where the oracle's own decision lies within
+    `rank_margin` (relative) of its threshold — fp64 rounding of sigma near eps ||A|| is of
+    order u/eps.  Returns (n_rank_mismatch_unexplained, n_tag_mismatch_unexplained, stats)."""
+    B = ex["blocks"]
+    lr = (B["storage"] == 0) & (Ho.storage == 0)
+    rk = B["rank"].astype(np.int64)
+    bad_r = lr & (rk != Ho.rank) & (Ho.margin > rank_margin)
+    same_r = lr & (rk == Ho.rank)
+    bad_t = same_r & (B["tag"].astype(np.int64) != Ho.tag) & (Ho.tag_margin > tag_margin)
+    st = dict(n_lr=int(lr.sum()), rank_diff=int((lr & (rk != Ho.rank)).sum()),
+              tag_diff=int((same_r & (B["tag"] != Ho.tag)).sum()),
+              storage_diff=int((B["storage"] != Ho.storage).sum()))
+    return int(bad_r.sum()), int(bad_t.sum()), st
+
+
+def gpu_matvec(H, x: np.ndarray) -> np.ndarray:
+    import torch
+    from paper_2604_09147_b200 import hh
+    xd = torch.from_numpy(np.asfortranarray(x).reshape(x.shape[0], -1, order="F").T.copy()).cuda().T
+    yd = torch.empty_like(xd.T).T
+    hh.hh_matvec(H, xd, yd, xd.shape[1])
+    torch.cuda.synchronize()
+    return yd.cpu().numpy()
+
+
+def oracle_build(P, cfg, pset=None, s=None, keep_exact=False):
+    return HM.build(P, cfg["kernel"], cfg["scale"], cfg["eps"], cfg["eta"], cfg["leaf"],
+                    cfg["s"] if s is None else s, cfg["pset"] if pset is None else pset, keep_exact=keep_exact)
+
+
+def rel2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b)) if np.linalg.norm(b) else float(np.linalg.norm(a))

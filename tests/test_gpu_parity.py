@@ -1,0 +1,165 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.  Needs a B200."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import dense as D
+from oracle import formats as F
+from oracle import metrics as M
+from oracle import partition as PT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import parity_lib as PL  # noqa: E402
+from paper_2604_09147_b200 import hh  # noqa: E402
+
+SMALL = ["2d_tiny", "2d_fig8_e4", "2d_fig8_e2", "3d_small_inv_r", "3d_small_exp"]
+
+
+@pytest.fixture(scope="module", params=SMALL)
+def built(request):
+    cfg = W.SMALL_CONFIGS[request.param]
+    P = W.make_points(cfg)
+    H = PL.gpu_build(P, cfg)
+    ex = PL.export(H)
+    Ho = PL.oracle_build(P, cfg, keep_exact=True)
+    return request.param, cfg, P, H, ex, Ho
+
+
+def test_check1a_partition_bit_exact(built):
+    _, cfg, P, H, ex, Ho = built
+    PL.check_partition(ex, Ho)
+
+
+def test_check1b_ranks_and_tags(built):
+    name, cfg, P, H, ex, Ho = built
+    bad_r, bad_t, st = PL.rank_tag_parity(ex, Ho)
+    print(name, st)
+    assert bad_r == 0 and bad_t == 0, st
+    assert st["rank_diff"] <= max(1, st["n_lr"] // 1000), st
+    # ||H~||^2 agrees with the oracle's Alg. 4 value
+    assert abs(ex["info"]["norm2"] - Ho.norm2) <= 1e-12 * Ho.norm2
+
+
+def test_check1c_packing_function(built):
+    _, cfg, P, H, ex, Ho = built
+    PL.check_packing(ex)
+
+
+def test_check2_matvec_vs_oracle_on_exported_factors(built):
+    _, cfg, P, H, ex, Ho = built
+    lay = PL.check_packing(ex)
+    for nrhs in sorted({1, cfg["nrhs"], 3, 16}):
+        x = W.make_rhs(cfg, nrhs)
+        y = PL.gpu_matvec(H, x)
+        yo = PL.oracle_matvec_on_export(ex, lay, x)
+        for c in range(nrhs):
+            assert PL.rel2(y[:, c], yo[:, c]) <= 1e-12, (nrhs, c, PL.rel2(y[:, c], yo[:, c]))
+
+
+def test_check3_and_4_error_vs_dense(built):
+    name, cfg, P, H, ex, Ho = built
+    x = W.make_rhs(cfg)
+    y = PL.gpu_matvec(H, x)
+    Ax, fro2 = D.dense_apply(P, cfg["kernel"], cfg["scale"], x)
+    e = M.e_mv(Ax, y, np.sqrt(fro2), x)[0]
+    assert e <= 10 * cfg["eps"], e                                   # check (3)
+    L, ell = ex["info"]["L"], cfg["s"]
+    info = ex["info"]
+    bound = M.thm44_factor(L, ell, info["c_far"], info["c_nbr"], info["c_sib"]) * cfg["eps"]
+    assert e <= bound                                                # Thm 4.4, measured constants
+    # check (4): mixed vs uniform-fp64 H_h, same partition
+    H64 = PL.gpu_build(P, cfg, pset=W.P_FP64)
+    y64 = PL.gpu_matvec(H64, x)
+    e64 = M.e_mv(Ax, y64, np.sqrt(fro2), x)[0]
+    B = ex["blocks"]
+    lv = B["level"][(B["storage"] == 0) & (B["rank"] > 0)].astype(float)
+    assert e - e64 <= 2 * cfg["eps"] * np.sqrt(np.sum(2.0 ** (-cfg["d"] * lv))) + 1e-15
+    assert e64 <= 10 * cfg["eps"]
+
+
+def test_global_error_thm42(built):
+    name, cfg, P, H, ex, Ho = built
+    lay = PL.check_packing(ex)
+    err2 = fro2 = 0.0
+    from oracle.kernels import block as kb
+    perm = ex["perm"].astype(np.int64)
+    for i0, i1, j0, j1, kind, payload in PL.exported_blocks(ex, lay):
+        A, _ = kb(P, perm[i0:i1], perm[j0:j1], cfg["kernel"], cfg["scale"])
+        fro2 += float(np.sum(A * A))
+        if kind == "lr":
+            E = A - payload[0] @ payload[1].T
+            err2 += float(np.sum(E * E))
+    info = ex["info"]
+    e = np.sqrt(err2 / fro2)
+    assert e <= M.thm42_factor(info["L"], cfg["s"], info["c_far"], info["c_nbr"], info["c_sib"]) * cfg["eps"]
+
+
+def test_determinism_bitwise(built):
+    _, cfg, P, H, ex, Ho = built
+    x = W.make_rhs(cfg, 2)
+    y1 = PL.gpu_matvec(H, x)
+    y2 = PL.gpu_matvec(H, x)
+    assert np.array_equal(y1, y2)
+
+
+def test_rounding_routines_match_oracle():
+    rng = np.random.default_rng(5)
+    base = rng.standard_normal(5000) * np.exp2(rng.integers(-140, 130, 5000))
+    for tag in (F.FP32, F.FP16, F.BF16):
+        r = F.round_rne(base, tag)
+        fin = np.isfinite(r) & (r != 0)
+        m, emin, _ = F.PARAMS[tag]
+        _, e = np.frexp(np.abs(r[fin]))
+        q = np.ldexp(1.0, np.maximum(e - 1, emin) - m)       # spacing of the format at r
+        mids = r[fin] + np.sign(r[fin]) * q / 2               # exact rounding midpoints
+        xs = np.concatenate([base, mids, np.nextafter(mids, 0), np.nextafter(mids, np.inf), [65519.99, 65520, 0.1]])
+        xs = xs[np.isfinite(xs)]
+        got = hh.selftest_round(xs, tag)
+        ref = F.to_storage_bits(xs, tag).astype(np.uint32)
+        np.testing.assert_array_equal(got, ref)
+
+
+def test_edge_cases_single_leaf_zero_x_hodlr_and_pure_hs():
+    # L = 0: N <= leaf -> dense gemv
+    P = W.points_uniform(60, 3, 77)
+    cfg = dict(kernel=W.K_INV_R, scale=1.0, eps=1e-6, eta=1.0, leaf=64, s=0, pset=W.P_MIXED)
+    H = PL.gpu_build(P, cfg)
+    x = W.rhs(60, 2, 1, "normal")
+    A = D.dense_matrix(P, W.K_INV_R, 1.0)
+    assert PL.rel2(PL.gpu_matvec(H, x), A @ x) < 1e-14
+    assert np.all(PL.gpu_matvec(H, np.zeros((60, 1))) == 0)
+    # HODLR (s = 0) and pure H_s (NONE), uniform and mixed, ragged leaves
+    P = W.points_uniform(3000, 2, 78)
+    for s in (0, 1, PT.SWITCH_NONE):
+        for pset in (W.P_FP64, W.P_MIXED):
+            cfg = dict(kernel=W.K_LOG, scale=1.0, eps=1e-6, eta=1.0, leaf=24, s=s, pset=pset)
+            H = PL.gpu_build(P, cfg)
+            ex = PL.export(H)
+            Ho = PL.oracle_build(P, cfg)
+            PL.check_partition(ex, Ho)
+            bad_r, bad_t, st = PL.rank_tag_parity(ex, Ho)
+            assert bad_r == 0 and bad_t == 0, (s, pset, st)
+            lay = PL.check_packing(ex)
+            x = W.rhs(3000, 1, 2, "uniform_pm1")
+            assert PL.rel2(PL.gpu_matvec(H, x), PL.oracle_matvec_on_export(ex, lay, x)) <= 1e-12
+
+
+def test_invalid_arguments_are_rejected():
+    P = torch.from_numpy(W.points_uniform(100, 2, 1)).cuda()
+    with pytest.raises(hh.HHError) as e:
+        hh.hh_build(P, 0, 1.0, 1e-6, 1.0, 16, 99, W.P_MIXED)     # switch level > L
+    assert e.value.status == hh.HH_EINVAL
+    with pytest.raises(hh.HHError):
+        hh.hh_build(P, 0, 1.0, 1e-6, 1.0, 16, 2, W.P_FP32)       # no fp64
+    with pytest.raises(hh.HHError):
+        hh.hh_build(P, 0, 1.0, 0.0, 1.0, 16, 2, W.P_MIXED)       # eps
+    bad = P.clone()
+    bad[3, 0] = float("nan")
+    with pytest.raises(hh.HHError) as e:
+        hh.hh_build(bad, 0, 1.0, 1e-6, 1.0, 16, 2, W.P_MIXED)
+    assert e.value.status == hh.HH_ENUMERIC
