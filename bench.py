@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""bench.py — H_h matvec throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3d_large] [--nrhs 1]
+    python bench.py --impl reference ...          # the CPU oracle arm (rank 0 only)
+
+A "step" is one hh_matvec (a7 gather, a8 phase 1, a9 phase 2 + a10 scatter) over the
+resident H-hat of the workload; the build (a1-a6) happens before the timed region.
+value = stored bytes (factor bytes at storage width + dense fp64 bytes) x steps x ranks
+/ max-over-ranks device time, in GB/s; matvecs/s is reported beside it.
+Multi-GPU: replicas only (north_star: one GPU, no collectives) — every rank builds and
+applies its own copy, `scaling: weak`.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "H_h matvec GB/s (stored bytes/time) vs HBM peak; matvecs/s at 3D N=2^20"
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_sample(cfg: dict, target_bytes: float, seed: int = 0):
+    """A bounded sample of the workload for the CPU oracle: the oracle's own tree and
+    partition of the full point set, then a random sample of blocks (stratified by level,
+    weighted by stored bytes) compressed by the oracle's truncated SVD.  Returns Alg. 3 block
+    records and the sample's stored bytes (low-rank at 4 B/element = the workloads' dominant
+    fp32 tag, dense at 8 B)."""
+    from oracle import compress as OC
+    from oracle import kernels as OK
+    from oracle import partition as OP
+    from oracle import tree as OT
+    P = W.make_points(cfg)
+    tr = OT.build_tree(P, cfg["leaf"])
+    part = OP.build_partition(tr, cfg["eta"], cfg["s"])
+    rng = np.random.default_rng(seed)
+    sh = tr.d * (tr.L - part.level)
+    m = tr.leaf_start[(part.tgt + 1) << sh] - tr.leaf_start[part.tgt << sh]
+    n = tr.leaf_start[(part.src + 1) << sh] - tr.leaf_start[part.src << sh]
+    dense = (part.kind == OP.DIAG) | (part.kind == OP.LNBR)
+    # byte-weighted draw (low-rank bytes ~ p (m + n), dense m n); blocks whose SVD would take
+    # minutes on one core (side > 2048) are left out of the sample
+    w = np.where(dense, m * n, 16 * (m + n)).astype(float)
+    w[np.maximum(m, n) > 2048] = 0.0
+    order = rng.choice(len(part), size=min(len(part), 20000), replace=False, p=w / w.sum())
+    blocks, nbytes, picked = [], 0, 0
+    t_setup = time.perf_counter()
+    for b in order:
+        if nbytes >= target_bytes or time.perf_counter() - t_setup > 90:
+            break
+        l = int(part.level[b])
+        i0, i1 = tr.cluster(l, int(part.tgt[b]))
+        j0, j1 = tr.cluster(l, int(part.src[b]))
+        A, _ = OK.block(P, tr.perm[i0:i1], tr.perm[j0:j1], cfg["kernel"], cfg["scale"])
+        if part.kind[b] in (OP.DIAG,) or (part.kind[b] == OP.LNBR):
+            blocks.append((i0, i1, j0, j1, "dense", A))
+            nbytes += A.size * 8
+        else:
+            c = OC.lr_compress(A, cfg["eps"])
+            blocks.append((i0, i1, j0, j1, "lr", (c["U"].astype(np.float32).astype(np.float64),
+                                                  c["W"].astype(np.float32).astype(np.float64))))
+            nbytes += c["p"] * (A.shape[0] + A.shape[1]) * 4
+        picked += 1
+    return tr, blocks, nbytes
+
+
+def oracle_rate(cfg: dict, seconds: float, steps: int | None = None):
+    """Time the oracle's Alg. 3 (oracle.matvec.matvec_blocks, as it stands) over the sample."""
+    from oracle import matvec as OM
+    tr, blocks, nbytes = oracle_sample(cfg, target_bytes=float(os.environ.get("HH_ORACLE_SAMPLE_BYTES", 1.5e8)))
+    x = W.make_rhs(cfg, 1)
+    times = []
+    t_end = time.perf_counter() + seconds
+    k = 0
+    while (steps is None and (time.perf_counter() < t_end or k < 2)) or (steps is not None and k < steps):
+        t0 = time.perf_counter()
+        OM.matvec_blocks(cfg["N"], tr.perm, blocks, x)
+        times.append(time.perf_counter() - t0)
+        k += 1
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    return nbytes, times, cores, len(blocks)
+
+
+# ----------------------------------------------------------------------------- our arm
+def stored_split(ex):
+    """Algorithmic bytes streamed by phase 1 (W factors) and phase 2 (U factors + dense)."""
+    B = ex["blocks"]
+    ls = ex["leaf_start"]
+    d, L = ex["info"]["d"], ex["info"]["L"]
+    sh = d * (L - B["level"].astype(np.int64))
+    m = ls[(B["tgt"] + 1) << sh] - ls[B["tgt"] << sh]
+    n = ls[(B["src"] + 1) << sh] - ls[B["src"] << sh]
+    wb = np.array([8, 4, 2, 2])[B["tag"]]
+    lr = B["storage"] == 0
+    p = B["rank"].astype(np.int64)
+    w_bytes = int(np.sum((p * n * wb)[lr]))
+    u_bytes = int(np.sum((p * m * wb)[lr]))
+    d_bytes = int(np.sum((m * n * 8)[~lr]))
+    return w_bytes, u_bytes, d_bytes
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_2604_09147_b200 import hh
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = dict(W.CONFIGS[args.config])
+    if args.switch is not None:
+        cfg["s"] = args.switch
+    if args.pset is not None:
+        cfg["pset"] = args.pset
+    nrhs = args.nrhs
+    P = torch.from_numpy(W.make_points(cfg)).to(dev)
+    t0 = time.time()
+    H = hh.hh_build(P, cfg["kernel"], cfg["scale"], cfg["eps"], cfg["eta"], cfg["leaf"], cfg["s"], cfg["pset"])
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    del P
+    info = hh.hh_info(H)
+    ex = hh.hh_export(H, tables=True, arenas=False)
+    w_bytes, u_bytes, d_bytes = stored_split(ex)
+    del ex
+    stored = info["stored_bytes"]
+    x_h = W.make_rhs(cfg, nrhs)
+    x = torch.from_numpy(x_h.T.copy()).to(dev).T          # column-major (N, nrhs)
+    y = torch.empty_like(x.T).T
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = stored < 4 * l2
+    fbuf = torch.empty(int(2 * l2 // 4) + 1, dtype=torch.float32, device=dev) if flush else None
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        hh.hh_matvec(H, x, y, nrhs)
+    torch.cuda.synchronize()
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+        tdist.barrier()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    time.sleep(0.3)
+    hh.hh_matvec_timing(H)                        # reset
+    hh.hh_matvec_profile(H, True)
+    launches0 = hh.kernel_launches()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if dist:
+        tdist.barrier()
+    t_wall = time.perf_counter()
+    for k in range(args.steps):
+        if flush:
+            fbuf.fill_(float(k))
+        evs[k][0].record(stream)
+        hh.hh_matvec(H, x, y, nrhs)
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    launches = hh.kernel_launches() - launches0
+    hh.hh_matvec_profile(H, False)
+    phase_ms, nchunks = hh.hh_matvec_timing(H)
+    clocks = clk.stop()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+    per_step = ms / args.steps
+    value = stored * args.steps * world / (ms / 1e3) / 1e9
+    # e2e: host buffers through hh_matvec_host (H2D of x, matvec, D2H of y inside)
+    e2e = None
+    if not args.no_e2e:
+        xp = torch.from_numpy(x_h.T.copy()).pin_memory()
+        yp = torch.empty_like(xp).pin_memory()
+        import ctypes as C
+        for _ in range(2):
+            hh.lib.hh_matvec_host(H.ptr, C.c_void_p(xp.data_ptr()), C.c_void_p(yp.data_ptr()), nrhs,
+                                  C.c_void_p(stream.cuda_stream))
+        ee = []
+        for k in range(max(3, args.steps // 2)):
+            if flush:
+                fbuf.fill_(float(k))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st = hh.lib.hh_matvec_host(H.ptr, C.c_void_p(xp.data_ptr()), C.c_void_p(yp.data_ptr()), nrhs,
+                                       C.c_void_p(stream.cuda_stream))
+            b.record(stream)
+            assert st == 0
+            torch.cuda.synchronize()
+            ee.append(a.elapsed_time(b))
+        e_ms = sum(ee) / len(ee)
+        if dist:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": round(stored * world / (e_ms / 1e3) / 1e9, 2), "unit": "GB/s",
+               "matvecs_per_s": round(world * 1e3 / e_ms, 3), "ms_per_step": round(e_ms, 4),
+               "h2d_bytes_per_step": int(8 * cfg["N"] * nrhs), "d2h_bytes_per_step": int(8 * cfg["N"] * nrhs)}
+    # roofline of the dominant kernel (phase 1 streams W, phase 2 streams U + dense)
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs")
+    peak, peak_src = (hbm, "measured (MEASURED_PEAKS.json hbm_gbs)") if hbm else (6650.0, "fallback (B200_PROFILING.md)")
+    p1_ms = phase_ms[1] / max(1, nchunks)
+    p2_ms = phase_ms[2] / max(1, nchunks)
+    kernels = {"phase1": (w_bytes, p1_ms), "phase2": (u_bytes + d_bytes, p2_ms)}
+    dom = max(kernels, key=lambda k: kernels[k][1])
+    alg_bytes, kms = kernels[dom]
+    achieved = alg_bytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tj.get(args.config, {}).get(dom)
+    except Exception:
+        pass
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(per_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "matvecs_per_s": round(world * args.steps / (ms / 1e3), 3),
+        "config": {"workload": args.config, "N": cfg["N"], "d": cfg["d"], "kernel": W.KERNEL_NAMES[cfg["kernel"]],
+                   "eps": cfg["eps"], "eta": cfg["eta"], "leaf_size": cfg["leaf"], "switch_level": cfg["s"],
+                   "precision_set": cfg["pset"], "nrhs": nrhs, "parallelism": f"replicas{world}",
+                   "stored_bytes": stored, "padded_bytes": info["padded_bytes"],
+                   "stored_bytes_by_tag": dict(zip(["fp64", "fp32", "fp16", "bf16", "dense_fp64"], info["stored_bytes_tag"])),
+                   "nblocks": info["nblocks"], "total_rank": info["total_rank"], "L": info["L"],
+                   "l2_policy": "flush (2x L2 write) before each step" if flush else "inputs larger than L2",
+                   "build_seconds": round(build_s, 2)},
+        "frac_of_hbm_peak": round(value / world / peak, 4),
+        "roofline": {"bound": "hbm", "kernel": f"k_phase{dom[-1]}", "achieved": round(achieved, 1),
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
+                     "phase_ms_per_step": {"gather": round(phase_ms[0] / max(1, nchunks), 4),
+                                           "phase1": round(p1_ms, 4), "phase2": round(p2_ms, 4)},
+                     "phase1_GBps": round(w_bytes / (p1_ms / 1e3) / 1e9, 1) if p1_ms else None,
+                     "phase2_GBps": round((u_bytes + d_bytes) / (p2_ms / 1e3) / 1e9, 1) if p2_ms else None},
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nbytes, times, cores, nblk = oracle_rate(cfg, seconds=args.cpu_seconds)
+        med = statistics.median(times)
+        line["cpu_baseline"] = {"value": round(nbytes / med / 1e9, 4), "unit": "GB/s", "cores": cores,
+                                "kind": "oracle",
+                                "sample": f"{nblk} blocks of {args.config} ({nbytes / 1e6:.1f} MB stored), oracle "
+                                          f"Alg. 3 (oracle/matvec.py) x{len(times)} passes, median",
+                                "matvecs_per_s_equiv": round(nbytes / med / stored, 6)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = W.CONFIGS[args.config]
+    # size of the workload's stored bytes is a property of the method; the reference arm
+    # reports the oracle's GB/s over its own bounded sample and the equivalent matvecs/s
+    # against the GPU build's stored bytes recorded in profiles/ (if present)
+    for _ in range(args.warmup):
+        pass
+    nbytes, times, cores, nblk = oracle_rate(cfg, seconds=0.0, steps=args.warmup + args.steps)
+    times = times[args.warmup:]
+    tot = sum(times)
+    value = nbytes * len(times) / tot / 1e9
+    line = {"metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(times), 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.config, "N": cfg["N"], "nrhs": args.nrhs,
+                       "sample": f"{nblk} blocks, {nbytes / 1e6:.1f} MB stored"},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{nblk} random blocks of {args.config} compressed by the oracle; one step = "
+                                       f"one oracle Alg. 3 pass over them"},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="3d_large", choices=list(W.CONFIGS))
+    ap.add_argument("--nrhs", type=int, default=1)
+    ap.add_argument("--switch", type=int, default=None)
+    ap.add_argument("--pset", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -124,6 +124,17 @@ hh_status hh_matvec(hh_handle H, const double *x, double *y, int32_t nrhs, void 
 hh_status hh_matvec_host(hh_handle H, const double *x_host, double *y_host, int32_t nrhs,
                          void *cuda_stream);
 
+/*
+ * hh_matvec_profile / hh_matvec_timing — optional per-phase device timing of hh_matvec (used
+ * by bench.py for the roofline).  While enabled, every hh_matvec records CUDA events on the
+ * caller's stream around its gather (a7), phase 1 (a8, incl. the combine of split columns)
+ * and phase 2 (a9 + fused scatter a10).  hh_matvec_timing synchronises on the last event and
+ * returns, summed over the matvec chunks recorded since the previous call, ms[0] = gather,
+ * ms[1] = phase 1, ms[2] = phase 2, ms[3] = their sum; *count = number of chunks (may be NULL).
+ */
+hh_status hh_matvec_profile(hh_handle H, int32_t enable);
+hh_status hh_matvec_timing(hh_handle H, double *ms, int64_t *count);
+
 /* Summary of a built handle (always available, host memory, filled by hh_info). */
 typedef struct {
   int32_t d, L, switch_level, kernel_kind;

@@ -4,4 +4,5 @@ The product is the C-ABI library ``libhh.so`` (include/hh.h, sources in ``csrc/`
 package holds the in-tree build script and the ctypes binding (``hh``).
 """
 from .hh import (EXPORTED, Handle, HHError, hh_build, hh_export, hh_free, hh_info, hh_matvec,  # noqa: F401
-                 hh_matvec_host, kernel_launches, selftest_round)
+                 hh_matvec_host, hh_matvec_profile, hh_matvec_timing, kernel_launches,
+                 selftest_round)

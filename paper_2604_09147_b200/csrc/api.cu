@@ -244,6 +244,10 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
     }
     I.d_bytes = H->d_bytes;
     I.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (getenv("HH_PROFILE_BUILD")) {
+      print_build_profile();
+      fprintf(stderr, "[hh build profile] total %.2fs retries=%lld\n", I.build_seconds, (long long)I.n_retry);
+    }
     *out = H;
     return HH_OK;
   } catch (const Error &e) {
@@ -278,16 +282,48 @@ hh_status hh_matvec_host(hh_handle H, const double *x_host, double *y_host, int3
   g_err.clear();
   if (!H || !x_host || !y_host) return fail(HH_EINVAL, "NULL pointer");
   if (nrhs < 1) return fail(HH_EINVAL, "nrhs must be >= 1");
+  if (H->ledger) return fail(HH_EINVAL, "ledger-only handle has no factors");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   try {
-    DBuf dx, dy;
     const size_t bytes = sizeof(double) * (size_t)H->N * nrhs;
-    dx.alloc(bytes);
-    dy.alloc(bytes);
-    HH_CUDA(cudaMemcpyAsync(dx.p, x_host, bytes, cudaMemcpyHostToDevice, st));
-    run_matvec(H, dx.as<double>(), dy.as<double>(), nrhs, st);
-    HH_CUDA(cudaMemcpyAsync(y_host, dy.p, bytes, cudaMemcpyDeviceToHost, st));
+    if (H->hx.bytes < bytes) {  // handle-owned staging, grown on demand
+      H->hx.alloc(bytes);
+      H->hy.alloc(bytes);
+    }
+    HH_CUDA(cudaMemcpyAsync(H->hx.p, x_host, bytes, cudaMemcpyHostToDevice, st));
+    run_matvec(H, H->hx.as<double>(), H->hy.as<double>(), nrhs, st);
+    HH_CUDA(cudaMemcpyAsync(y_host, H->hy.p, bytes, cudaMemcpyDeviceToHost, st));
     HH_CUDA(cudaStreamSynchronize(st));
+    return HH_OK;
+  } catch (const Error &e) {
+    return fail(e.st, e.what());
+  }
+}
+
+hh_status hh_matvec_profile(hh_handle H, int32_t enable) {
+  if (!H) return fail(HH_EINVAL, "NULL handle");
+  H->prof = enable != 0;
+  return HH_OK;
+}
+
+hh_status hh_matvec_timing(hh_handle H, double *ms, int64_t *count) {
+  g_err.clear();
+  if (!H || !ms) return fail(HH_EINVAL, "NULL pointer");
+  try {
+    for (int i = 0; i < 4; ++i) ms[i] = 0.0;
+    const size_t n = H->prof_ev.size() / 4;
+    if (n) HH_CUDA(cudaEventSynchronize(H->prof_ev.back()));
+    for (size_t c = 0; c < n; ++c) {
+      float t[3];
+      for (int i = 0; i < 3; ++i) HH_CUDA(cudaEventElapsedTime(&t[i], H->prof_ev[4 * c + i], H->prof_ev[4 * c + i + 1]));
+      for (int i = 0; i < 3; ++i) {
+        ms[i] += t[i];
+        ms[3] += t[i];
+      }
+    }
+    for (auto e : H->prof_ev) cudaEventDestroy(e);
+    H->prof_ev.clear();
+    if (count) *count = (int64_t)n;
     return HH_OK;
   } catch (const Error &e) {
     return fail(e.st, e.what());

@@ -40,5 +40,6 @@ void build_plan(hh_matrix *H, std::vector<P1Item> &items, std::vector<P1Entry> &
                 std::vector<Combine> &combines, int64_t &npartial, std::vector<P2Chunk> &chunks,
                 std::vector<P2Leaf> &leaves);
 void run_matvec(hh_matrix *H, const double *x, double *y, int nrhs, cudaStream_t st);
+void print_build_profile();
 
 }  // namespace hh

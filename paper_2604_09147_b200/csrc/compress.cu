@@ -589,8 +589,25 @@ KernelFn make_kernel_fn(const hh_kernel &kk) {
 
 // Runs the compression pipeline on `jobs` (pass 1: results only; pass 2: also write the
 // rounded factors).  Returns one result per job.
+// Optional build profile (HH_PROFILE_BUILD=1): per-stage device time accumulated over batches.
+static const char *kStage[8] = {"gemm_Y", "qr_Y", "gemm_Z", "qr_Z", "jacobi", "resid", "decide", "factors"};
+double g_stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+int64_t g_stage_batches = 0;
+void print_build_profile() {
+  fprintf(stderr, "[hh build profile] batches=%lld", (long long)g_stage_batches);
+  for (int i = 0; i < 8; ++i) fprintf(stderr, " %s=%.1fms", kStage[i], g_stage_ms[i]);
+  fprintf(stderr, "\n");
+}
+
 void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob> &jobs, bool write,
                   const Arenas *ar, std::vector<CompressResult> &res, cudaStream_t st, size_t ws_budget) {
+  static const bool prof = getenv("HH_PROFILE_BUILD") != nullptr;
+  cudaEvent_t ev[9];
+  if (prof)
+    for (int i = 0; i < 9; ++i) HH_CUDA(cudaEventCreate(&ev[i]));
+  auto mark = [&](int i) {
+    if (prof) HH_CUDA(cudaEventRecord(ev[i], st));
+  };
   res.assign(jobs.size(), CompressResult{});
   const KernelFn K = make_kernel_fn(H->kernel);
   const double delta = 1e-9;
@@ -666,37 +683,54 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
     const Task *dA = taskb.as<Task>(), *dB = dA + tA.size(), *dR = dB + tB.size();
     double *ws = wsb.as<double>();
     CBlk *db = blkb.as<CBlk>();
+    mark(0);
     // Y = A Omega
     for (size_t t0 = 0; t0 < tA.size(); t0 += 65535) {
       dim3 g((unsigned)std::min<size_t>(65535, tA.size() - t0), gy);
       k_gemm_gen<0><<<g, THREADS, 0, st>>>(dA + t0, db, ws, pts, H->N, H->d, K);
       HH_LAUNCHED();
     }
+    mark(1);
     k_qr<true><<<nb, THREADS, 0, st>>>(db, ws, 0);
     HH_LAUNCHED();
+    mark(2);
     // Z = A^T Q (and a copy for the R-only QR)
     for (size_t t0 = 0; t0 < tB.size(); t0 += 65535) {
       dim3 g((unsigned)std::min<size_t>(65535, tB.size() - t0), gy);
       k_gemm_gen<1><<<g, THREADS, 0, st>>>(dB + t0, db, ws, pts, H->N, H->d, K);
       HH_LAUNCHED();
     }
+    mark(3);
     k_qr<false><<<nb, THREADS, 0, st>>>(db, ws, 1);
     HH_LAUNCHED();
+    mark(4);
     const int jsm = std::min(kmax, JAC_SMEM_K);
     const size_t jsmem = sizeof(double) * (size_t)jsm * jsm;
     HH_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * JAC_SMEM_K * JAC_SMEM_K)));
     k_jacobi<<<nb, THREADS, jsmem, st>>>(db, ws);
     HH_LAUNCHED();
+    mark(5);
     k_resid<<<(unsigned)tR.size(), THREADS, 0, st>>>(dR, db, ws, pts, H->N, H->d, K, partb.as<double>());
     HH_LAUNCHED();
+    mark(6);
     k_decide<<<(nb + 127) / 128, 128, 0, st>>>(db, nb, ws, partb.as<double>(), H->eps, delta);
     HH_LAUNCHED();
+    mark(7);
     Arenas a{};
     if (write) a = *ar;
     k_factors<<<nb, THREADS, 0, st>>>(db, ws, write ? 1 : 0, a);
     HH_LAUNCHED();
+    mark(8);
     HH_CUDA(cudaMemcpyAsync(blks.data(), blkb.p, sizeof(CBlk) * nb, cudaMemcpyDeviceToHost, st));
     HH_CUDA(cudaStreamSynchronize(st));
+    if (prof) {
+      for (int i = 0; i < 8; ++i) {
+        float ms = 0;
+        HH_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+        g_stage_ms[i] += ms;
+      }
+      ++g_stage_batches;
+    }
     for (int i = 0; i < nb; ++i) {
       CompressResult &r = res[pos + i];
       const CBlk &c = blks[i];

@@ -105,6 +105,13 @@ struct hh_matrix {
   int64_t n_p1_items = 0, n_p2_leaves = 0, n_combines = 0, n_partials = 0;
   hh::DBuf v;        // [(N + ztotal) * 16] doubles
   hh::DBuf partial;  // [n_partials * 16] doubles
+  hh::DBuf hx, hy;   // staging for hh_matvec_host
+  // optional per-phase timing of the matvec (hh_matvec_profile)
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;  // 4 per matvec chunk: start, after gather, after phase 1, after phase 2
   // statistics
   hh_info_t info{};
+  ~hh_matrix() {
+    for (auto e : prof_ev) cudaEventDestroy(e);
+  }
 };

@@ -302,9 +302,18 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   HH_CUDA(cudaGetDevice(&dev));
   HH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   double *v = H->v.as<double>();
+  cudaEvent_t ev[4];
+  auto mark = [&](int i) {
+    if (!H->prof) return;
+    HH_CUDA(cudaEventCreate(&ev[i]));
+    HH_CUDA(cudaEventRecord(ev[i], st));
+    H->prof_ev.push_back(ev[i]);
+  };
+  mark(0);
   // a7 gather
   k_gather<NR><<<nsm * 8, 256, 0, st>>>(H->d_perm.as<int32_t>(), x + (int64_t)col0 * H->N, H->N, H->N, v);
   HH_LAUNCHED();
+  mark(1);
   // a8 phase 1
   if (H->n_p1_items > 0) {
     P1Args a{};
@@ -331,6 +340,7 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
       HH_LAUNCHED();
     }
   }
+  mark(2);
   // a9 + a10 phase 2 with fused scatter
   P2Args b{};
   b.leaves = H->p2_leaves.as<P2Leaf>();
@@ -355,6 +365,7 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     k_phase2<NR><<<(unsigned)grid2, THREADS, sm2, st>>>(b);
     HH_LAUNCHED();
   }
+  mark(3);
 }
 
 void run_matvec(hh_matrix *H, const double *x, double *y, int nrhs, cudaStream_t st) {

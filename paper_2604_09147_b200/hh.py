@@ -86,14 +86,17 @@ def _load():
     lib.hh_last_error.restype = C.c_char_p
     lib.hh_kernel_launches.restype = C.c_int64
     lib.hh_selftest_round.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]
-    for f in ("hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_selftest_round"):
+    lib.hh_matvec_profile.argtypes = [C.c_void_p, C.c_int32]
+    lib.hh_matvec_timing.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    for f in ("hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_selftest_round",
+              "hh_matvec_profile", "hh_matvec_timing"):
         getattr(lib, f).restype = C.c_int
     return lib
 
 
 lib = _load()
 EXPORTED = ["hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_last_error",
-            "hh_kernel_launches", "hh_selftest_round"]
+            "hh_kernel_launches", "hh_selftest_round", "hh_matvec_profile", "hh_matvec_timing"]
 
 
 def _check(st):
@@ -195,6 +198,18 @@ def export_arena(H: Handle, arena: int, off: int, length: int) -> np.ndarray:
     e.arena, e.arena_off, e.arena_len, e.arena_dst = arena, off, length, buf.ctypes.data
     _check(lib.hh_export(H.ptr, C.byref(e)))
     return buf
+
+
+def hh_matvec_profile(H: Handle, enable: bool = True):
+    _check(lib.hh_matvec_profile(H.ptr, 1 if enable else 0))
+
+
+def hh_matvec_timing(H: Handle) -> tuple[list, int]:
+    """Device ms of (gather, phase 1, phase 2, total) summed since the last call, and count."""
+    ms = (C.c_double * 4)()
+    n = C.c_int64()
+    _check(lib.hh_matvec_timing(H.ptr, ms, C.byref(n)))
+    return list(ms), int(n.value)
 
 
 def hh_free(H: Handle):
