@@ -1,4 +1,5 @@
 // api.cpp — the C-ABI (include/hh.h): argument validation, build orchestration, export.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -55,6 +56,7 @@ void compress_all(hh_matrix *H, const double *pts, const std::vector<int64_t> &l
   int64_t retries = 0;
   std::vector<CompressJob> retry;
   std::vector<CompressResult> res;
+  std::vector<std::vector<int>> cls_p(64 * 8);
   while (pos < lr.size() || !retry.empty()) {
     jobs.clear();
     if (!retry.empty()) {
@@ -76,7 +78,8 @@ void compress_all(hh_matrix *H, const double *pts, const std::vector<int64_t> &l
       const int64_t n = H->leaf_start[(H->src[b] + 1) << sh] - H->leaf_start[H->src[b] << sh];
       const int kfull = (int)std::min<int64_t>(std::min(m, n), KMAX);
       if (!r.ok && r.k < kfull) {
-        retry.push_back(CompressJob{b, std::min(kfull, 2 * r.k)});
+        const int kn = r.k < 64 ? 2 * r.k : ((r.k + r.k / 2 + 7) / 8) * 8;
+        retry.push_back(CompressJob{b, std::min(kfull, kn)});
         ++retries;
         continue;
       }
@@ -87,8 +90,15 @@ void compress_all(hh_matrix *H, const double *pts, const std::vector<int64_t> &l
       H->nb2[b] = r.nb2;
       H->tot[b] = r.tot;
       H->maxabs[b] = r.maxabs;
-      int &ke = kest[H->level[b] * 8 + H->kind[b]];
-      ke = std::max(ke, std::min(KMAX, ((r.p + 24 + 7) / 8) * 8));
+      cls_p[H->level[b] * 8 + H->kind[b]].push_back(r.p);
+    }
+    // next sketch width per (level, kind): 90th percentile of the ranks just accepted + 12
+    for (size_t c = 0; c < cls_p.size(); ++c) {
+      std::vector<int> &v = cls_p[c];
+      if (v.empty()) continue;
+      std::nth_element(v.begin(), v.begin() + (v.size() * 9) / 10, v.end());
+      kest[c] = std::min(KMAX, std::max(16, ((v[(v.size() * 9) / 10] + 12 + 7) / 8) * 8));
+      v.clear();
     }
   }
   H->info.n_retry = retries;

@@ -280,16 +280,17 @@ __global__ void __launch_bounds__(THREADS) k_qr(CBlk *blks, double *ws, int whic
 // ---------------------------------------------------------------- Hestenes Jacobi
 // M = T^T (k x k) where T = upper triangle of the QR of Z (stored in Zc, ld n).
 // Output: s (descending) at os, Ut (k x k, columns = left singular vectors of T^T) at ot.
-constexpr int JAC_SMEM_K = 160;
+constexpr int JAC_SMEM_K = 168;   // 168^2 doubles = 220.5 KiB of shared memory
+constexpr int JT = 1024;          // Jacobi block size (32 warps -> 32 rotation pairs in flight)
 
-__global__ void __launch_bounds__(THREADS) k_jacobi(CBlk *blks, double *ws) {
+__global__ void __launch_bounds__(JT) k_jacobi(CBlk *blks, double *ws) {
   extern __shared__ double smem[];
   CBlk &B = blks[blockIdx.x];
   const int k = B.k, n = B.n;
   double *M = (k <= JAC_SMEM_K) ? smem : ws + B.oy;  // Y no longer needed (Q formed)
   const double *R = ws + B.ozc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int64_t e = tid; e < (int64_t)k * k; e += THREADS) {
+  for (int64_t e = tid; e < (int64_t)k * k; e += JT) {
     int i = (int)(e % k), j = (int)(e / k);
     M[e] = (j <= i) ? R[(int64_t)i * n + j] : 0.0;  // M[i][j] = T[j][i]
   }
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(THREADS) k_jacobi(CBlk *blks, double *ws) {
     __syncthreads();
     int myrot = 0;
     for (int r = 0; r < kk - 1; ++r) {
-      for (int q = warp; q < kk / 2; q += THREADS / 32) {
+      for (int q = warp; q < kk / 2; q += JT / 32) {
         auto player = [&](int pos) { return pos == 0 ? 0 : (pos - 1 + r) % (kk - 1) + 1; };
         int a = player(q), b = player(kk - 1 - q);
         if (a >= k || b >= k) continue;
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(THREADS) k_jacobi(CBlk *blks, double *ws) {
   double *sig = ws + B.os;
   double *Ut = ws + B.ot;
   double *norms = ws + B.otau;  // tau no longer needed
-  for (int j = warp; j < k; j += THREADS / 32) {
+  for (int j = warp; j < k; j += JT / 32) {
     double s = 0;
     for (int i = lane; i < k; i += 32) s = __fma_rn(M[(int64_t)j * k + i], M[(int64_t)j * k + i], s);
 #pragma unroll
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(THREADS) k_jacobi(CBlk *blks, double *ws) {
     if (lane == 0) norms[j] = sqrt(s);
   }
   __syncthreads();
-  for (int j = tid; j < k; j += THREADS) {
+  for (int j = tid; j < k; j += JT) {
     double nj = norms[j];
     int rk = 0;
     for (int i = 0; i < k; ++i) {
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(THREADS) k_jacobi(CBlk *blks, double *ws) {
     norms[k + j] = (double)rk;  // stash rank (tau area has >= 2k doubles)
   }
   __syncthreads();
-  for (int64_t e = tid; e < (int64_t)k * k; e += THREADS) {
+  for (int64_t e = tid; e < (int64_t)k * k; e += JT) {
     int i = (int)(e % k), j = (int)(e / k);
     int rk = (int)norms[k + j];
     double nj = norms[j];
@@ -483,7 +484,20 @@ __global__ void k_decide(CBlk *blks, int nb, const double *ws, const double *par
   double nb2 = 0;
   for (int j = 0; j < max(best, 0); ++j) nb2 = __fma_rn(s[j], s[j], nb2);
   B.nb2 = nb2;
-  B.ok = (best >= 0) && (full || R <= delta * thr);
+  // Exactness of the decision: the SVD tail satisfies gpu_tail(q) - R <= tail(q) <= gpu_tail(q)
+  // for every q (interlacing of sigma(Q^T A) with sigma(A)).  Hence the SVD rank equals
+  // `best` when gpu_tail(best - 1) - R > thr, i.e. R is below the gap at the decision; a
+  // relative guard of 1e-9 absorbs rounding.  R <= 1e-10 tot keeps nb2 (which feeds the
+  // precision tag, Eq. 4.4) accurate to 1e-10.  Otherwise the sketch is widened.
+  bool exact = false;
+  if (best == 0) {
+    exact = true;
+  } else if (best > 0) {
+    double tprev = R;  // gpu_tail(best - 1) = R + sum_{j >= best-1} s_j^2
+    for (int j = k - 1; j >= best - 1; --j) tprev += s[j] * s[j];
+    exact = (tprev - R > thr * (1.0 + delta)) && (R <= 1e-10 * tot);
+  }
+  B.ok = (best >= 0) && (full || exact);
 }
 
 // ---------------------------------------------------------------- factors
@@ -707,7 +721,7 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
     const int jsm = std::min(kmax, JAC_SMEM_K);
     const size_t jsmem = sizeof(double) * (size_t)jsm * jsm;
     HH_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * JAC_SMEM_K * JAC_SMEM_K)));
-    k_jacobi<<<nb, THREADS, jsmem, st>>>(db, ws);
+    k_jacobi<<<nb, JT, jsmem, st>>>(db, ws);
     HH_LAUNCHED();
     mark(5);
     k_resid<<<(unsigned)tR.size(), THREADS, 0, st>>>(dR, db, ws, pts, H->N, H->d, K, partb.as<double>());
