@@ -164,7 +164,8 @@ hh_status hh_info(hh_handle H, hh_info_t *info);
 typedef struct {
   int64_t tgt, src;           /* Morton codes of target / source cluster at `level` */
   int64_t zoff;               /* offset in z (low-rank), -1 otherwise */
-  int64_t w_off;              /* byte offset in W[tag] (rank > 0), -1 otherwise */
+  int64_t w_off;              /* byte offset of the block's source panel in W[tag] (rank > 0), -1 otherwise */
+  int64_t wcol;               /* first column of the block inside that panel, -1 otherwise */
   int64_t ucol;               /* first column inside the target's leaf streams, -1 otherwise */
   int64_t d_off;              /* byte offset in the dense arena (dense blocks), -1 otherwise */
   double nb2;                 /* ||H~_b||_F^2 = sum of kept sigma^2 (low-rank) */

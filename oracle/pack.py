@@ -7,8 +7,13 @@ computed here with the offsets the GPU build exported, bit for bit.
 
 Layout (byte offsets; ALIGN = 16):
   z     : low-rank blocks ordered by (level, tgt, tag, src); zoff = exclusive prefix sum of p.
-  W[g]  : tag-g low-rank blocks with p > 0 ordered by (level, src, tgt); W_b is n_b x p_b
-          column-major; each block starts at a multiple of ALIGN.
+  W[g]  : source panels.  Tag-g low-rank blocks with p > 0 ordered by (level, src, tgt); a
+          run of equal (level, src) is one panel: an n x P matrix (n = |src cluster|, P = sum
+          of the run's ranks) whose columns are the blocks' W_b columns in that order
+          (wcol[b] = first column of b).  The panel is cut into column tiles of CT = 256
+          columns (the last one narrower); each tile is stored row-major (element (r, j) of a
+          tile of width ct at r * ct + j) and starts at a multiple of ALIGN; tiles follow each
+          other in column order.  w_off[b] = byte offset of the panel's first tile.
   U[g]  : one stream per leaf R (Morton order), starting at a multiple of ALIGN; inside,
           for levels l = 1..L, the tag-g low-rank blocks with target anc_l(R) in src order
           contribute their rows U_b[R, :] as an |R| x p_b column-major slab.  ucol[b] is the
@@ -24,6 +29,7 @@ import numpy as np
 from . import formats as F
 
 ALIGN = 16
+CT = 256          # W panel column-tile width
 LR, DENSE = 0, 1
 
 
@@ -60,15 +66,30 @@ def pack(leaf_start, d, L, level, tgt, src, rank, tag, storage):
     zoff[order] = np.cumsum(pz) - pz
     ztotal = int(pz.sum())
 
-    # W arenas
+    # W arenas: panels of column tiles
     w_off = np.full(nb, -1, np.int64)
+    wcol = np.full(nb, -1, np.int64)
+    wpanel = np.full(nb, -1, np.int64)
     w_bytes = np.zeros(4, np.int64)
     for g in range(4):
         idx = np.nonzero(lr & (tag == g) & (rank > 0))[0]
         order = idx[np.lexsort((tgt[idx], src[idx], level[idx]))]
-        sz = align_up(n_b[order] * rank[order] * F.BYTES[g])
-        w_off[order] = np.cumsum(sz) - sz
-        w_bytes[g] = int(sz.sum())
+        off = 0
+        k = 0
+        while k < order.size:
+            e = k
+            while e < order.size and level[order[e]] == level[order[k]] and src[order[e]] == src[order[k]]:
+                e += 1
+            run = order[k:e]
+            P = int(rank[run].sum())
+            wcol[run] = np.cumsum(rank[run]) - rank[run]
+            wpanel[run] = P
+            w_off[run] = off
+            n = int(n_b[run[0]])
+            for c0 in range(0, P, CT):
+                off += int(align_up(n * min(CT, P - c0) * F.BYTES[g]))
+            k = e
+        w_bytes[g] = off
 
     # U arenas: per-group column totals G[l][(t, g)], ucol per block
     ucol = np.full(nb, -1, np.int64)
@@ -115,9 +136,22 @@ def pack(leaf_start, d, L, level, tgt, src, rank, tag, storage):
     within = np.cumsum(sizes) - sizes
     first_of_leaf = np.searchsorted(tgt[o], tgt[o], side="left")
     d_off[o] = d_leaf_off[tgt[o]] + (within - within[first_of_leaf])
-    return dict(zoff=zoff, ztotal=ztotal, w_off=w_off, w_bytes=w_bytes, ucol=ucol,
+    return dict(zoff=zoff, ztotal=ztotal, w_off=w_off, wcol=wcol, wpanel=wpanel, w_bytes=w_bytes, ucol=ucol,
                 u_leaf_off=u_leaf_off, d_off=d_off, d_leaf_off=d_leaf_off,
-                m=m_b, n=n_b, i0=i0, j0=j0)
+                m=m_b, n=n_b, i0=i0, j0=j0, rank=rank)
+
+
+def w_offsets(layout, b, g):
+    """Byte offsets in W[g] of the n x p elements W_b[r, c] of low-rank block b (p > 0)."""
+    n, w = int(layout["n"][b]), F.BYTES[g]
+    P, c0 = int(layout["wpanel"][b]), int(layout["wcol"][b])
+    p = int(layout["rank"][b])
+    r = np.arange(n, dtype=np.int64)[:, None]
+    pc = c0 + np.arange(p, dtype=np.int64)[None, :]      # panel columns
+    t = pc // CT                                          # tile
+    ct = np.minimum(CT, P - t * CT)                       # tile width
+    tile_start = int(layout["w_off"][b]) + t * int(align_up(n * CT * w))   # all earlier tiles are full
+    return tile_start + (r * ct + (pc - t * CT)) * w
 
 
 def unpack_block(layout, b, leaf_start, d, L, level, tgt, rank, tag, storage, arenas):
@@ -135,8 +169,10 @@ def unpack_block(layout, b, leaf_start, d, L, level, tgt, rank, tag, storage, ar
     if p == 0:
         return "lr", (np.zeros((m, 0)), np.zeros((n, 0)))
     w = F.BYTES[g]
-    wo = int(layout["w_off"][b])
-    W = F.from_storage_bytes(arenas[("W", g)][wo:wo + n * p * w], g).reshape(p, n).T
+    offs = w_offsets(layout, b, g)
+    raw = arenas[("W", g)]
+    elem = np.stack([raw[offs + k] for k in range(w)], axis=-1).reshape(-1)
+    W = F.from_storage_bytes(elem, g).reshape(n, p)
     U = np.zeros((m, p))
     l = int(level[b])
     i0 = int(layout["i0"][b])

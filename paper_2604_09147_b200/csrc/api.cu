@@ -212,24 +212,20 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
         if (H->storage[b] == STORE_DENSE) dn2.push_back((int64_t)b);
       run_dense(H, pts.as<double>(), dn2, true, st);
       // matvec plan + workspace
-      std::vector<P1Item> items;
-      std::vector<P1Entry> entries;
-      std::vector<Combine> combines;
-      std::vector<P2Chunk> chunks;
+      std::vector<P1Tile> tiles;
+      std::vector<int32_t> zmap;
+      std::vector<P2Seg> segs;
       std::vector<P2Leaf> leaves;
-      int64_t npart = 0;
-      build_plan(H, items, entries, combines, npart, chunks, leaves);
-      h2d(H->p1_items, items, st);
-      h2d(H->p1_entries, entries, st);
-      h2d(H->combines, combines, st);
-      h2d(H->p2_chunks, chunks, st);
+      build_plan(H, tiles, zmap, segs, leaves);
+      h2d(H->p1_tiles, tiles, st);
+      h2d(H->zmap, zmap, st);
+      h2d(H->p2_segs, segs, st);
       h2d(H->p2_leaves, leaves, st);
-      H->n_p1_items = (int64_t)items.size();
-      H->n_combines = (int64_t)combines.size();
+      H->n_p1_tiles = (int64_t)tiles.size();
       H->n_p2_leaves = (int64_t)leaves.size();
-      H->n_partials = npart;
-      H->partial.alloc(sizeof(double) * 16 * std::max<int64_t>(1, npart));
-      H->v.alloc(sizeof(double) * 16 * (size_t)(N + H->ztotal));
+      H->v.alloc(sizeof(double) * 16 * (size_t)(N + H->ztotal) + 64);
+      H->ctr.alloc(64);
+      HH_CUDA(cudaMemsetAsync(H->ctr.p, 0, 64, st));
       HH_CUDA(cudaStreamSynchronize(st));
     }
     // info
@@ -365,6 +361,7 @@ hh_status hh_export(hh_handle H, hh_export_t *out) {
         r.src = H->src[b];
         r.zoff = H->zoff.empty() ? -1 : H->zoff[b];
         r.w_off = H->w_off.empty() ? -1 : H->w_off[b];
+        r.wcol = H->wcol.empty() ? -1 : H->wcol[b];
         r.ucol = H->ucol.empty() ? -1 : H->ucol[b];
         r.d_off = H->d_off.empty() ? -1 : H->d_off[b];
         r.nb2 = H->nb2.empty() ? 0 : H->nb2[b];

@@ -35,7 +35,8 @@ struct CBlk {
   int64_t task0;       // first resid task
   int64_t gid;         // block id (RNG stream)
   // pass-2 output placement
-  int64_t w_off, ucol;
+  int64_t w_off, ucol;  // W panel byte offset; first column inside the target's leaf streams
+  int64_t wcol, wP, wts; // column inside the W panel, panel width, full-tile stride (bytes)
   int32_t tag, pad;
   // results
   double R, tot, nb2, maxabs;
@@ -502,7 +503,8 @@ __global__ void k_decide(CBlk *blks, int nb, const double *ws, const double *par
 
 // ---------------------------------------------------------------- factors
 // U = Q Ut[:, :p] (m x p), W = Z Ut[:, :p] (n x p).  Pass 1: max |entry|.  Pass 2: round to
-// the block's tag and store (W: n x p col-major at w_off; U rows into the target's leaf streams).
+// the block's tag and store (W: columns wcol.. of its source panel, row-major column tiles;
+// U rows into the target's leaf streams).
 __device__ __forceinline__ void store_tagged(uint8_t *base, int64_t elem, int tag, double v) {
   switch (tag) {
     case TAG_FP64:
@@ -564,7 +566,9 @@ __global__ void __launch_bounds__(THREADS) k_factors(CBlk *blks, const double *w
           if (write) {
             const int c = c0 + q;
             if (side == 1) {
-              store_tagged(ar.W[B.tag] + B.w_off, (int64_t)c * B.n + i, B.tag, acc[q]);
+              const int64_t pc = B.wcol + c, t = pc / W_CT, j = pc - t * W_CT;
+              const int64_t ct = min((int64_t)W_CT, B.wP - t * W_CT);
+              store_tagged(ar.W[B.tag] + B.w_off + t * B.wts, (int64_t)i * ct + j, B.tag, acc[q]);
             } else {
               const int64_t pos = B.i0 + i;
               const int32_t R = ar.leaf_of[pos];
@@ -667,6 +671,9 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
         c.tag = H->tag[b];
         c.w_off = H->w_off[b];
         c.ucol = H->ucol[b];
+        c.wcol = H->wcol[b];
+        c.wP = H->wpanel[b];
+        c.wts = align_up((int64_t)c.n * W_CT * tag_bytes(c.tag));
       }
       blks.push_back(c);
       ++end;

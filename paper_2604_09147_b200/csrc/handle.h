@@ -36,40 +36,34 @@ template <class T> void h2d(DBuf &b, const std::vector<T> &v, cudaStream_t s) {
   if (!v.empty()) HH_CUDA(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
 }
 
-// Phase-1 work item: a contiguous, 16-B aligned window of one W arena plus the entries
-// (column groups) it holds.  Phase-2 work: per leaf, a list of column chunks.
-struct P1Item {
-  int64_t src;        // byte offset in W[tag] (multiple of 16)
-  uint32_t nbytes;    // multiple of 16
-  uint16_t tag, pad;
-  uint32_t e0, e1;    // entries [e0, e1)
+// W panels: for each (tag, level, source cluster J) the tag's low-rank blocks
+// with source J, in target order, form one |J| x P_J panel (P_J = sum of their ranks) split
+// into column tiles of width <= W_CT, each stored row-major and 16-B aligned.
+constexpr int W_CT = 256;
+
+// Phase-1 work item: one column tile of one W panel (all |J| rows).
+struct P1Tile {
+  int64_t src;        // byte offset of the tile in W[tag] (multiple of 16)
+  int64_t x0;         // v index (tree position) of the panel's row 0
+  int64_t zbase;      // index into zmap of the tile's column 0
+  int32_t n;          // rows (= |J|)
+  int16_t ct;         // columns (1..W_CT)
+  int16_t tag;
 };
-struct P1Entry {
-  uint32_t soff;      // byte offset of the first column inside the staged window
-  uint32_t nrows;     // column length (rows of W_b, or a row piece)
-  uint32_t ncols;
-  uint32_t pad;
-  int64_t x0;         // v index (tree position) of row 0
-  int64_t out;        // z index of the first column (>= 0) or ~slot for a partial piece
-};
-struct P2Chunk {
-  int64_t src;        // byte offset (multiple of 16) in U[tag] or D
-  uint32_t nbytes;    // multiple of 16
-  uint32_t lead;      // bytes skipped at the start of the window
-  uint32_t ncols;
-  uint16_t tag;       // 0..3, dense uses 0 (fp64) with arena flag
-  uint16_t dense;     // 1 -> dense arena
-  int64_t vbeg;       // v index of column 0's vector entry
+// Phase-2 work: per leaf R, a list of segments; a segment is `ncols` contiguous |R|-row
+// columns (column-major) of U[tag] or of the dense arena, multiplied by v[vbeg ...].
+struct P2Seg {
+  int64_t src;        // byte offset of column 0 in U[tag] (or D); multiple of the element size
+  int64_t vbeg;       // v index of column 0's vector entry (z for U, x~ for dense)
+  int32_t ncols;
+  int16_t tag;        // 0..3 (dense: 0)
+  int16_t dense;      // 1 -> dense arena
 };
 struct P2Leaf {
   int64_t r0;         // first tree position
   int32_t nr;         // rows
   int32_t pad;
-  int64_t c0, c1;     // chunks [c0, c1)
-};
-struct Combine {      // z[zi] = sum_{s in [s0, s1)} partial[s]
-  int64_t zi;
-  int64_t s0, s1;
+  int64_t s0, s1;     // segments [s0, s1)
 };
 
 }  // namespace hh
@@ -91,7 +85,7 @@ struct hh_matrix {
   std::vector<uint8_t> level, kind, tag, storage;
   std::vector<int64_t> tgt, src;
   std::vector<int32_t> rank, kfinal;
-  std::vector<int64_t> zoff, w_off, ucol, d_off;
+  std::vector<int64_t> zoff, w_off, wcol, wpanel, ucol, d_off;
   std::vector<double> nb2, tot, maxabs;
   std::vector<int64_t> u_leaf_off;        // [4*(ncell+1)]
   std::vector<int64_t> d_leaf_off;        // [ncell+1]
@@ -101,10 +95,10 @@ struct hh_matrix {
   hh::DBuf W[4], U[4], D;
   int64_t w_bytes[4] = {0, 0, 0, 0}, u_bytes[4] = {0, 0, 0, 0}, d_bytes = 0;
   // matvec plan
-  hh::DBuf p1_items, p1_entries, p2_chunks, p2_leaves, combines;
-  int64_t n_p1_items = 0, n_p2_leaves = 0, n_combines = 0, n_partials = 0;
-  hh::DBuf v;        // [(N + ztotal) * 16] doubles
-  hh::DBuf partial;  // [n_partials * 16] doubles
+  hh::DBuf p1_tiles, zmap, p2_segs, p2_leaves;
+  int64_t n_p1_tiles = 0, n_p2_leaves = 0;
+  hh::DBuf v;        // [(N + ztotal) * 16] doubles (+ slack for 16-B aligned superset copies)
+  hh::DBuf ctr;      // work counters of the persistent matvec kernels (zeroed by the gather)
   hh::DBuf hx, hy;   // staging for hh_matvec_host
   // optional per-phase timing of the matvec (hh_matvec_profile)
   bool prof = false;

@@ -113,21 +113,43 @@ void compute_layout(hh_matrix *H) {
     }
     H->ztotal = z;
   }
-  // W[g]: tag-g low-rank blocks with p > 0 in (level, src, tgt) order, 16-B aligned
+  // W[g]: panels.  Tag-g low-rank blocks with p > 0 in (level, src, tgt) order; a run of
+  // equal (level, src) is one panel of |J| rows and P = sum p columns; block b occupies panel
+  // columns [wcol, wcol + p).  Column tiles of W_CT columns (the last one narrower), each
+  // stored row-major, start at multiples of ALIGN.  w_off[b] = byte offset of b's panel.
+  H->wcol.assign(nb, -1);
+  H->wpanel.assign(nb, -1);
   {
     std::vector<size_t> idx;
     for (size_t b = 0; b < nb; ++b)
       if (is_lr(b) && H->rank[b] > 0) idx.push_back(b);
     std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t c) {
+      if (H->tag[a] != H->tag[c]) return H->tag[a] < H->tag[c];
       if (H->level[a] != H->level[c]) return H->level[a] < H->level[c];
       if (H->src[a] != H->src[c]) return H->src[a] < H->src[c];
       return H->tgt[a] < H->tgt[c];
     });
     int64_t off[4] = {0, 0, 0, 0};
-    for (size_t b : idx) {
-      const int g = H->tag[b];
-      H->w_off[b] = off[g];
-      off[g] += align_up(Nn[b] * H->rank[b] * tag_bytes(g));
+    size_t i = 0;
+    while (i < idx.size()) {
+      size_t e = i;
+      const size_t b0 = idx[i];
+      int64_t P = 0;
+      while (e < idx.size() && H->tag[idx[e]] == H->tag[b0] && H->level[idx[e]] == H->level[b0] &&
+             H->src[idx[e]] == H->src[b0]) {
+        const size_t b = idx[e];
+        H->wcol[b] = P;
+        P += H->rank[b];
+        ++e;
+      }
+      const int g = H->tag[b0];
+      for (size_t k = i; k < e; ++k) {
+        H->w_off[idx[k]] = off[g];
+        H->wpanel[idx[k]] = P;
+      }
+      const int64_t n = Nn[b0];
+      for (int64_t c0 = 0; c0 < P; c0 += W_CT) off[g] += align_up(n * std::min<int64_t>(W_CT, P - c0) * tag_bytes(g));
+      i = e;
     }
     for (int g = 0; g < 4; ++g) H->w_bytes[g] = off[g];
   }
@@ -220,84 +242,63 @@ void compute_layout(hh_matrix *H) {
 }
 
 // ----------------------------------------------------------------- matvec work plan
-constexpr int64_t STAGE_BYTES = 16384;
-
-void build_plan(hh_matrix *H, std::vector<P1Item> &items, std::vector<P1Entry> &entries,
-                std::vector<Combine> &combines, int64_t &npartial, std::vector<P2Chunk> &chunks,
+// Phase 1: one item per W column tile, largest first (the kernels take items from a work
+// counter, so big tiles start early).  zmap[zbase + c] = z index of tile column c.
+// Phase 2: per leaf, dense segments then per tag the levels' U column groups; leaves with
+// the most bytes first.
+void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &zmap, std::vector<P2Seg> &segs,
                 std::vector<P2Leaf> &leaves) {
   const size_t nb = H->level.size();
   const int d = H->d, L = H->L;
   const int64_t N = H->N;
-  items.clear();
-  entries.clear();
-  combines.clear();
-  chunks.clear();
+  tiles.clear();
+  zmap.clear();
+  segs.clear();
   leaves.clear();
-  npartial = 0;
-  // ---- phase 1: W arenas in storage order
+  HH_REQUIRE(H->ztotal < INT32_MAX, HH_EUNSUPPORTED, "total rank exceeds 2^31");
+  // ---- phase 1
   std::vector<size_t> idx;
   for (size_t b = 0; b < nb; ++b)
     if (H->storage[b] == STORE_LR && H->rank[b] > 0) idx.push_back(b);
   std::sort(idx.begin(), idx.end(), [&](size_t a, size_t c) {
     if (H->tag[a] != H->tag[c]) return H->tag[a] < H->tag[c];
-    return H->w_off[a] < H->w_off[c];
+    if (H->w_off[a] != H->w_off[c]) return H->w_off[a] < H->w_off[c];
+    return H->wcol[a] < H->wcol[c];
   });
-  P1Item cur{};
-  bool open = false;
-  auto flush = [&]() {
-    if (open && cur.e1 > cur.e0) items.push_back(cur);
-    open = false;
-  };
-  for (size_t b : idx) {
-    const int g = H->tag[b];
-    const int w = tag_bytes(g);
-    int64_t j0, n, i0, m;
-    cluster_range(H, H->level[b], H->src[b], j0, n);
-    cluster_range(H, H->level[b], H->tgt[b], i0, m);
-    const int p = H->rank[b];
-    const int64_t bytes = n * p * w, pbytes = align_up(bytes);
-    if (open && (cur.tag != g || (int64_t)cur.nbytes + pbytes > STAGE_BYTES)) flush();
-    if (pbytes <= STAGE_BYTES) {
-      if (!open) {
-        cur = P1Item{H->w_off[b], 0, (uint16_t)g, 0, (uint32_t)entries.size(), (uint32_t)entries.size()};
-        open = true;
-      }
-      entries.push_back(P1Entry{(uint32_t)(H->w_off[b] - cur.src), (uint32_t)n, (uint32_t)p, 0, j0, H->zoff[b]});
-      cur.nbytes += (uint32_t)pbytes;
-      cur.e1 = (uint32_t)entries.size();
-      continue;
+  std::vector<int64_t> tbytes;
+  size_t i = 0;
+  while (i < idx.size()) {
+    size_t e = i;
+    while (e < idx.size() && H->tag[idx[e]] == H->tag[idx[i]] && H->w_off[idx[e]] == H->w_off[idx[i]]) ++e;
+    const size_t b0 = idx[i];
+    const int g = H->tag[b0];
+    int64_t j0, n;
+    cluster_range(H, H->level[b0], H->src[b0], j0, n);
+    const int64_t P = H->wpanel[b0];
+    // panel column -> z index
+    std::vector<int32_t> pz;
+    pz.reserve(P);
+    for (size_t k = i; k < e; ++k)
+      for (int c = 0; c < H->rank[idx[k]]; ++c) pz.push_back((int32_t)(H->zoff[idx[k]] + c));
+    int64_t off = H->w_off[b0];
+    for (int64_t c0 = 0; c0 < P; c0 += W_CT) {
+      const int64_t ct = std::min<int64_t>(W_CT, P - c0);
+      tiles.push_back(P1Tile{off, j0, (int64_t)zmap.size(), (int32_t)n, (int16_t)ct, (int16_t)g});
+      tbytes.push_back(n * ct * tag_bytes(g));
+      zmap.insert(zmap.end(), pz.begin() + c0, pz.begin() + c0 + ct);
+      off += align_up(n * ct * tag_bytes(g));
     }
-    flush();
-    const int64_t cb = n * w;
-    if (cb + 32 <= STAGE_BYTES) {  // runs of whole columns
-      const int64_t cpi = (STAGE_BYTES - 32) / cb;
-      for (int64_t c0 = 0; c0 < p; c0 += cpi) {
-        const int64_t c1 = std::min<int64_t>(p, c0 + cpi);
-        const int64_t s = H->w_off[b] + c0 * cb, e = H->w_off[b] + c1 * cb;
-        const int64_t sa = s / ALIGN * ALIGN, ea = align_up(e);
-        items.push_back(P1Item{sa, (uint32_t)(ea - sa), (uint16_t)g, 0, (uint32_t)entries.size(), (uint32_t)entries.size() + 1});
-        entries.push_back(P1Entry{(uint32_t)(s - sa), (uint32_t)n, (uint32_t)(c1 - c0), 0, j0, H->zoff[b] + c0});
-      }
-    } else {  // a column longer than a stage: row pieces + fixed-order combine
-      const int64_t rpi = ((STAGE_BYTES - 32) / w) / 32 * 32;
-      for (int64_t c = 0; c < p; ++c) {
-        Combine cm{H->zoff[b] + c, npartial, npartial};
-        for (int64_t r0 = 0; r0 < n; r0 += rpi) {
-          const int64_t r1 = std::min(n, r0 + rpi);
-          const int64_t s = H->w_off[b] + (c * n + r0) * w, e = H->w_off[b] + (c * n + r1) * w;
-          const int64_t sa = s / ALIGN * ALIGN, ea = align_up(e);
-          items.push_back(P1Item{sa, (uint32_t)(ea - sa), (uint16_t)g, 0, (uint32_t)entries.size(), (uint32_t)entries.size() + 1});
-          entries.push_back(P1Entry{(uint32_t)(s - sa), (uint32_t)(r1 - r0), 1, 0, j0 + r0, ~npartial});
-          ++npartial;
-        }
-        cm.s1 = npartial;
-        combines.push_back(cm);
-      }
-    }
+    i = e;
   }
-  flush();
-  // ---- phase 2: per leaf, per tag, per level groups; then dense blocks
-  // group (level, tgt, tag) -> (zbeg, P)
+  {
+    std::vector<size_t> ord(tiles.size());
+    for (size_t k = 0; k < ord.size(); ++k) ord[k] = k;
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t c) { return tbytes[a] > tbytes[c]; });
+    std::vector<P1Tile> t2(tiles.size());
+    for (size_t k = 0; k < ord.size(); ++k) t2[k] = tiles[ord[k]];
+    tiles.swap(t2);
+  }
+  // ---- phase 2: group (level, tgt, tag) -> (zbeg, P)
   std::vector<std::vector<int64_t>> gz(L + 1), gp(L + 1);
   for (int l = 0; l <= L; ++l) {
     gz[l].assign((size_t)4 << (d * l), -1);
@@ -309,29 +310,20 @@ void build_plan(hh_matrix *H, std::vector<P1Item> &items, std::vector<P1Entry> &
       if (gz[H->level[b]][key] < 0) gz[H->level[b]][key] = H->zoff[b];
       gp[H->level[b]][key] += H->rank[b];
     }
-  // dense blocks by target leaf
   std::vector<std::vector<size_t>> dense(H->ncell);
   for (size_t b = 0; b < nb; ++b)
     if (H->storage[b] == STORE_DENSE) dense[H->tgt[b]].push_back(b);
-  auto add_cols = [&](int64_t base, int64_t nr, int64_t ncols, int w, int tag, int isdense, int64_t vbeg) {
-    const int64_t cb = nr * w;
-    const int64_t cpc = std::max<int64_t>(1, (STAGE_BYTES - 32) / cb);
-    for (int64_t c0 = 0; c0 < ncols; c0 += cpc) {
-      const int64_t c1 = std::min(ncols, c0 + cpc);
-      const int64_t s = base + c0 * cb, e = base + c1 * cb;
-      const int64_t sa = s / ALIGN * ALIGN, ea = align_up(e);
-      chunks.push_back(P2Chunk{sa, (uint32_t)(ea - sa), (uint32_t)(s - sa), (uint32_t)(c1 - c0), (uint16_t)tag,
-                               (uint16_t)isdense, vbeg + c0});
-    }
-  };
+  std::vector<int64_t> lbytes;
   for (int64_t R = 0; R < H->ncell; ++R) {
     const int64_t r0 = H->leaf_start[R], nr = H->leaf_start[R + 1] - r0;
     if (nr == 0) continue;
-    P2Leaf lf{r0, (int32_t)nr, 0, (int64_t)chunks.size(), 0};
+    P2Leaf lf{r0, (int32_t)nr, 0, (int64_t)segs.size(), 0};
+    int64_t bytes = 0;
     for (const size_t b : dense[R]) {
       int64_t j0, n;
       cluster_range(H, H->level[b], H->src[b], j0, n);
-      add_cols(H->d_off[b], nr, n, 8, TAG_FP64, 1, j0);
+      segs.push_back(P2Seg{H->d_off[b], j0, (int32_t)n, (int16_t)TAG_FP64, 1});
+      bytes += nr * n * 8;
     }
     for (int g = 0; g < 4; ++g) {
       const int w = tag_bytes(g);
@@ -341,12 +333,22 @@ void build_plan(hh_matrix *H, std::vector<P1Item> &items, std::vector<P1Entry> &
         const size_t key = (size_t)(R >> (d * (L - l))) * 4 + g;
         const int64_t P = gp[l][key];
         if (P == 0) continue;
-        add_cols(base + col * nr * w, nr, P, w, g, 0, N + gz[l][key]);
+        segs.push_back(P2Seg{base + col * nr * w, N + gz[l][key], (int32_t)P, (int16_t)g, 0});
+        bytes += nr * P * w;
         col += P;
       }
     }
-    lf.c1 = (int64_t)chunks.size();
+    lf.s1 = (int64_t)segs.size();
     leaves.push_back(lf);
+    lbytes.push_back(bytes);
+  }
+  {
+    std::vector<size_t> ord(leaves.size());
+    for (size_t k = 0; k < ord.size(); ++k) ord[k] = k;
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t c) { return lbytes[a] > lbytes[c]; });
+    std::vector<P2Leaf> l2(leaves.size());
+    for (size_t k = 0; k < ord.size(); ++k) l2[k] = leaves[ord[k]];
+    leaves.swap(l2);
   }
 }
 

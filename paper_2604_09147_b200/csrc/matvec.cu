@@ -1,16 +1,23 @@
 // matvec.cu — §8(a) rows a7–a10: the hot path  y = H-hat x  (Alg. 3).
 //
-//   a7  gather:   v[t] = x[perm[t]]  (tree order, RHS-interleaved)
-//   a8  phase 1:  z_b = W_b^T x_J  for every low-rank block — streams the W arenas
+//   a7  gather:   v[t] = x[perm[t]]  (tree order, RHS-interleaved); also zeroes the work
+//                 counters of the two persistent kernels
+//   a8  phase 1:  z_b = W_b^T x_J for every low-rank block.  W is stored as per-source
+//                 panels: for a source cluster J all blocks b with src J form
+//                 one |J| x P_J matrix, cut into column tiles of <= 256 columns stored
+//                 row-major.  One work item = one tile; thread c of the CTA owns tile column
+//                 c and accumulates it over all |J| rows, so z needs no second pass.
 //   a9  phase 2:  per leaf R (one owner, fixed order, no atomics):
-//                 y_R = sum_dense D_RJ x_J + sum_{levels, tags} U_{R,l,g} z_{l,g}
+//                 y_R = sum_dense D_RJ x_J + sum_{tags, levels} U_{R,l,g} z_{l,g}
 //   a10 scatter:  fused into the phase-2 epilogue, y[perm[t]] = y~[t]
 // "Compute in working precision u": stored fp32/fp16/bf16 values are
 // up-converted exactly and accumulated in fp64.
 //
-// Both phases are persistent kernels with a producer warp that streams 16-B aligned arena
-// windows into a shared-memory ring with cp.async.bulk (TMA bulk copies, mbarrier
-// complete_tx) and 8 consumer warps that compute from shared memory.
+// Both phases are persistent kernels (grid = resident CTAs) that take work items from a
+// counter.  One producer thread streams each item through a ring of shared-memory stages
+// with cp.async.bulk (TMA bulk copies completing on an mbarrier): the factor window (<= 16
+// KiB) AND the matching vector slice (x~ rows for phase 1, z entries for phase 2) plus a
+// small descriptor, so the 8 consumer warps never touch global memory in their inner loops.
 #include <algorithm>
 #include <vector>
 
@@ -20,14 +27,37 @@ namespace hh {
 
 namespace mv {
 
-constexpr int STAGES = 6;
-constexpr int STAGE_BYTES = 16384;
 constexpr int NCW = 8;                 // consumer warps
-constexpr int THREADS = 32 * (NCW + 1);
+constexpr int NCT = NCW * 32;          // consumer threads
+constexpr int THREADS = NCT + 32;      // + one producer warp
+constexpr int WDATA = 16384;           // factor bytes per stage
+constexpr int WBUF = WDATA + 32;       // + 16-B alignment slack on both ends
+constexpr int META = 64;
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
+template <int NR> struct Geo {
+  static constexpr int XDATA = NR <= 2 ? 2048 : 8192;     // vector bytes per stage
+  static constexpr int XELEMS = XDATA / 8;                // doubles (rows x NR)
+  static constexpr int XBUF = XDATA + 32;
+  static constexpr int STAGE = WBUF + XBUF + META;
+  static constexpr int STAGES = NR == 2 ? 5 : 6;
+  static constexpr size_t smem(bool red) {
+    return (size_t)STAGES * STAGE + 2 * STAGES * sizeof(uint64_t) + (red ? sizeof(double) * NCT * NR : 0);
+  }
+};
+
+// Stage descriptor written by the producer before it arrives on the stage's full barrier.
+struct Meta {
+  int32_t kind;      // 0 = work, 1 = end of stream
+  int32_t wlead;     // bytes between the staged window start and element 0
+  int32_t xlead;
+  int32_t r0, r1;    // phase 1: rows [r0, r1) of the tile;  phase 2: columns [r0, r1) of the segment
+  int32_t flags;     // phase 2: bit 0 = last stage of the leaf
+  int32_t a, b;      // phase 1: ct, tag;  phase 2: nr, tag | dense << 8
+  int64_t p, q;      // phase 1: zbase, n;  phase 2: leaf r0, -
+};
+static_assert(sizeof(Meta) <= META, "meta");
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -60,10 +90,30 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory"); }
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory"); }
+
+// Copy [src, src + bytes) as the enclosing 16-B aligned window; returns the lead offset.
+__device__ __forceinline__ int stage_copy(uint8_t *dst, const uint8_t *src, int64_t bytes, uint64_t *bar,
+                                          uint64_t pol, uint32_t &tx) {
+  const uintptr_t s = (uintptr_t)src, sa = s & ~(uintptr_t)15, ea = (s + bytes + 15) & ~(uintptr_t)15;
+  if (bytes > 0) {
+    bulk_g2s(dst, (const void *)sa, (uint32_t)(ea - sa), bar, pol);
+    tx += (uint32_t)(ea - sa);
+  }
+  return (int)(s - sa);
+}
+__device__ __forceinline__ uint32_t window_bytes(const uint8_t *src, int64_t bytes) {
+  const uintptr_t s = (uintptr_t)src;
+  return bytes > 0 ? (uint32_t)(((s + bytes + 15) & ~(uintptr_t)15) - (s & ~(uintptr_t)15)) : 0u;
+}
 
 template <int TAG>
-__device__ __forceinline__ double ld_up(const uint8_t *base, int64_t i) {
+__device__ __forceinline__ double ld_up(const uint8_t *base, int i) {
   if (TAG == TAG_FP64) return reinterpret_cast<const double *>(base)[i];
   if (TAG == TAG_FP32) return (double)reinterpret_cast<const float *>(base)[i];
   if (TAG == TAG_FP16) return (double)__half2float(reinterpret_cast<const __half *>(base)[i]);
@@ -73,7 +123,8 @@ __device__ __forceinline__ double ld_up(const uint8_t *base, int64_t i) {
 // --------------------------------------------------------------------------- gather
 template <int NR>
 __global__ void k_gather(const int32_t *__restrict__ perm, const double *__restrict__ x, int64_t N, int64_t ldx,
-                         double *__restrict__ v) {
+                         double *__restrict__ v, int *ctr) {
+  if (blockIdx.x == 0 && threadIdx.x < 2) ctr[threadIdx.x] = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = perm[t];
 #pragma unroll
@@ -83,103 +134,131 @@ __global__ void k_gather(const int32_t *__restrict__ perm, const double *__restr
 
 // --------------------------------------------------------------------------- phase 1
 struct P1Args {
-  const P1Item *items;
-  const P1Entry *entries;
-  int64_t nitems;
+  const P1Tile *tiles;
+  const int32_t *zmap;
+  int64_t ntiles;
   const uint8_t *W[4];
   double *v;          // [x~ (N) ; z] x NR
-  double *partial;    // [slots] x NR
   int64_t N;
+  int *ctr;
 };
 
+// rows [0, nrows) of the staged window; thread (c, q) takes rows q, q + Q, ...
 template <int TAG, int NR>
-__device__ __forceinline__ void p1_column(const uint8_t *col, int nrows, const double *__restrict__ xv, int lane,
-                                          double (&acc)[NR]) {
+__device__ __forceinline__ void p1_rows(const uint8_t *wst, const double *xst, int nrows, int ct, int c, int q,
+                                        int Q, double (&acc)[NR]) {
+  constexpr int w = TAG == TAG_FP64 ? 8 : (TAG == TAG_FP32 ? 4 : 2);
+  const uint8_t *col = wst + c * w;
+  const int stride = ct;
+#pragma unroll 4
+  for (int i = q; i < nrows; i += Q) {
+    const double a = ld_up<TAG>(col, i * stride);
 #pragma unroll
-  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
-  for (int r = lane; r < nrows; r += 32) {
-    const double w = ld_up<TAG>(col, r);
-#pragma unroll
-    for (int q = 0; q < NR; ++q) acc[q] = __fma_rn(w, __ldg(xv + (int64_t)r * NR + q), acc[q]);
+    for (int k = 0; k < NR; ++k) acc[k] = __fma_rn(a, xst[i * NR + k], acc[k]);
   }
-#pragma unroll
-  for (int q = 0; q < NR; ++q)
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
 }
 
 template <int NR>
 __global__ void __launch_bounds__(THREADS) k_phase1(P1Args a) {
+  using G = Geo<NR>;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
-  uint64_t *empty = full + STAGES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
+  uint64_t *empty = full + G::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < G::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (warp == NCW) {  // producer
-    if (lane == 0) {
-      const uint64_t pol = evict_first_policy();
-      int n = 0;
-      for (int64_t it = blockIdx.x; it < a.nitems; it += gridDim.x, ++n) {
-        const int s = n % STAGES;
-        if (n >= STAGES) mbar_wait(&empty[s], ((n / STAGES) & 1) ^ 1);
-        const P1Item I = a.items[it];
-        mbar_expect_tx(&full[s], I.nbytes);
-        bulk_g2s(smem + s * STAGE_BYTES, a.W[I.tag] + I.src, I.nbytes, &full[s], pol);
+  if (warp == NCW) {  // ------------------------------------------------ producer
+    if (lane != 0) return;
+    const uint64_t pol_w = evict_first_policy(), pol_x = evict_last_policy();
+    int n = 0;
+    int item = atomicAdd(a.ctr, 1);
+    while (item < a.ntiles) {
+      const P1Tile T = a.tiles[item];
+      const int nxt = atomicAdd(a.ctr, 1);
+      const int w = tag_bytes(T.tag);
+      const int rowb = T.ct * w;
+      const int rs = max(1, min(G::XELEMS / NR, WDATA / rowb));
+      const uint8_t *wbase = a.W[T.tag] + T.src;
+      const uint8_t *xbase = reinterpret_cast<const uint8_t *>(a.v + T.x0 * NR);
+      for (int r0 = 0; r0 < T.n; r0 += rs, ++n) {
+        const int r1 = min(T.n, r0 + rs);
+        const int s = n % G::STAGES;
+        if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
+        uint8_t *st = smem + s * G::STAGE;
+        const uint8_t *wsrc = wbase + (int64_t)r0 * rowb;
+        const int64_t wlen = (int64_t)(r1 - r0) * rowb;
+        const uint8_t *xsrc = xbase + (int64_t)r0 * NR * 8;
+        const int64_t xlen = (int64_t)(r1 - r0) * NR * 8;
+        Meta *m = reinterpret_cast<Meta *>(st + WBUF + G::XBUF);
+        m->kind = 0;
+        m->wlead = (int)((uintptr_t)wsrc & 15);
+        m->xlead = (int)((uintptr_t)xsrc & 15);
+        m->r0 = r0;
+        m->r1 = r1;
+        m->a = T.ct;
+        m->b = T.tag;
+        m->p = T.zbase;
+        m->q = T.n;
+        mbar_expect_tx(&full[s], window_bytes(wsrc, wlen) + window_bytes(xsrc, xlen));
+        uint32_t tx = 0;
+        stage_copy(st, wsrc, wlen, &full[s], pol_w, tx);
+        stage_copy(st + WBUF, xsrc, xlen, &full[s], pol_x, tx);
       }
+      item = nxt;
     }
+    const int s = n % G::STAGES;
+    if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
+    reinterpret_cast<Meta *>(smem + s * G::STAGE + WBUF + G::XBUF)->kind = 1;
+    mbar_arrive(&full[s]);
     return;
   }
-  int n = 0;
-  for (int64_t it = blockIdx.x; it < a.nitems; it += gridDim.x, ++n) {
-    const int s = n % STAGES;
-    const P1Item I = a.items[it];
-    mbar_wait(&full[s], (n / STAGES) & 1);
-    const uint8_t *stage = smem + s * STAGE_BYTES;
-    const int w = tag_bytes(I.tag);
-    int gc = 0;  // running column counter inside the item; warp gc % NCW owns column gc
-    for (uint32_t e = I.e0; e < I.e1; ++e) {
-      const P1Entry E = a.entries[e];
-      int c = (warp - gc % NCW + NCW) % NCW;
-      for (; c < (int)E.ncols; c += NCW) {
-        const uint8_t *col = stage + E.soff + (int64_t)c * E.nrows * w;
-        const double *xv = a.v + E.x0 * NR;
-        double acc[NR];
-        switch (I.tag) {
-          case TAG_FP64: p1_column<TAG_FP64, NR>(col, E.nrows, xv, lane, acc); break;
-          case TAG_FP32: p1_column<TAG_FP32, NR>(col, E.nrows, xv, lane, acc); break;
-          case TAG_FP16: p1_column<TAG_FP16, NR>(col, E.nrows, xv, lane, acc); break;
-          default: p1_column<TAG_BF16, NR>(col, E.nrows, xv, lane, acc); break;
-        }
-        if (lane == 0) {
-          double *out = E.out >= 0 ? a.v + (a.N + E.out + c) * NR : a.partial + (~E.out) * NR;
+  // --------------------------------------------------------------------- consumers
+  const int tid = threadIdx.x;
+  double acc[NR];
+  int32_t zi = 0;
+  for (int n = 0;; ++n) {
+    const int s = n % G::STAGES;
+    mbar_wait(&full[s], (n / G::STAGES) & 1);
+    const uint8_t *st = smem + s * G::STAGE;
+    const Meta m = *reinterpret_cast<const Meta *>(st + WBUF + G::XBUF);
+    if (m.kind) break;
+    const int ct = m.a;
+    const int Q = ct > 128 ? 1 : ct > 64 ? 2 : ct > 32 ? 4 : 8;   // row groups (power of two)
+    const int c = tid / Q, q = tid % Q;
+    const bool active = c < ct;
+    if (m.r0 == 0) {
 #pragma unroll
-          for (int q = 0; q < NR; ++q) out[q] = acc[q];
-        }
+      for (int k = 0; k < NR; ++k) acc[k] = 0.0;
+      if (active && q == 0) zi = a.zmap[m.p + c];
+    }
+    if (active) {
+      const uint8_t *wst = st + m.wlead;
+      const double *xst = reinterpret_cast<const double *>(st + WBUF + m.xlead);
+      const int nrows = m.r1 - m.r0;
+      switch (m.b) {
+        case TAG_FP64: p1_rows<TAG_FP64, NR>(wst, xst, nrows, ct, c, q, Q, acc); break;
+        case TAG_FP32: p1_rows<TAG_FP32, NR>(wst, xst, nrows, ct, c, q, Q, acc); break;
+        case TAG_FP16: p1_rows<TAG_FP16, NR>(wst, xst, nrows, ct, c, q, Q, acc); break;
+        default: p1_rows<TAG_BF16, NR>(wst, xst, nrows, ct, c, q, Q, acc); break;
       }
-      gc += E.ncols;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-  }
-}
-
-template <int NR>
-__global__ void k_combine(const Combine *__restrict__ cm, int64_t n, const double *__restrict__ partial, double *v,
-                          int64_t N) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const Combine C = cm[i];
+    if (m.r1 == m.q) {  // last stage of the tile: fixed-order reduction over the Q row groups
+      for (int o = 1; o < Q; o <<= 1)
 #pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      double s = 0.0;
-      for (int64_t k = C.s0; k < C.s1; ++k) s += partial[k * NR + q];
-      v[(N + C.zi) * NR + q] = s;
+        for (int k = 0; k < NR; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+      if (active && q == 0) {
+        double *out = a.v + (a.N + zi) * NR;
+#pragma unroll
+        for (int k = 0; k < NR; ++k) out[k] = acc[k];
+      }
     }
   }
 }
@@ -187,7 +266,7 @@ __global__ void k_combine(const Combine *__restrict__ cm, int64_t n, const doubl
 // --------------------------------------------------------------------------- phase 2
 struct P2Args {
   const P2Leaf *leaves;
-  const P2Chunk *chunks;
+  const P2Seg *segs;
   int64_t nleaves;
   const uint8_t *U[4];
   const uint8_t *D;
@@ -195,113 +274,145 @@ struct P2Args {
   const int32_t *perm;
   double *y;
   int64_t ldy;
+  int *ctr;
 };
 
+// columns [0, ncols) of the staged window; thread (row rr, group g) takes g, g + G, ...
 template <int TAG, int NR>
-__device__ __forceinline__ void p2_chunk(const uint8_t *stage, const P2Chunk &C, int nr, int rr, int g, int G,
-                                         const double *__restrict__ v, double (&acc)[NR]) {
-  const uint8_t *base = stage + C.lead;
-  const double *vv = v + C.vbeg * NR;
-  for (int c = g; c < (int)C.ncols; c += G) {
-    const double u = ld_up<TAG>(base, (int64_t)c * nr + rr);
+__device__ __forceinline__ void p2_cols(const uint8_t *ust, const double *zst, int ncols, int nr, int rr, int g, int G,
+                                        double (&acc)[NR]) {
+#pragma unroll 4
+  for (int c = g; c < ncols; c += G) {
+    const double u = ld_up<TAG>(ust, c * nr + rr);
 #pragma unroll
-    for (int q = 0; q < NR; ++q) acc[q] = __fma_rn(u, __ldg(vv + (int64_t)c * NR + q), acc[q]);
+    for (int k = 0; k < NR; ++k) acc[k] = __fma_rn(u, zst[c * NR + k], acc[k]);
   }
 }
 
 template <int NR>
 __global__ void __launch_bounds__(THREADS) k_phase2(P2Args a) {
+  using G = Geo<NR>;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
-  uint64_t *empty = full + STAGES;
-  double *red = reinterpret_cast<double *>(empty + STAGES);  // [NCW*32][NR]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
+  uint64_t *empty = full + G::STAGES;
+  double *red = reinterpret_cast<double *>(empty + G::STAGES);  // [NCT][NR]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < G::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (warp == NCW) {
-    if (lane == 0) {
-      const uint64_t pol = evict_first_policy();
-      int n = 0;
-      for (int64_t li = blockIdx.x; li < a.nleaves; li += gridDim.x) {
-        const P2Leaf Lf = a.leaves[li];
-        for (int64_t ci = Lf.c0; ci < Lf.c1; ++ci, ++n) {
-          const int s = n % STAGES;
-          if (n >= STAGES) mbar_wait(&empty[s], ((n / STAGES) & 1) ^ 1);
-          const P2Chunk C = a.chunks[ci];
-          mbar_expect_tx(&full[s], C.nbytes);
-          const uint8_t *src = (C.dense ? a.D : a.U[C.tag]) + C.src;
-          bulk_g2s(smem + s * STAGE_BYTES, src, C.nbytes, &full[s], pol);
+  if (warp == NCW) {  // ------------------------------------------------ producer
+    if (lane != 0) return;
+    const uint64_t pol_w = evict_first_policy(), pol_x = evict_last_policy();
+    int n = 0;
+    int li = atomicAdd(a.ctr + 1, 1);
+    while (li < a.nleaves) {
+      const P2Leaf Lf = a.leaves[li];
+      const int nxt = atomicAdd(a.ctr + 1, 1);
+      for (int64_t si = Lf.s0; si < Lf.s1; ++si) {
+        const P2Seg S = a.segs[si];
+        const int w = tag_bytes(S.tag);
+        const int colb = Lf.nr * w;
+        const int cs = max(1, min(G::XELEMS / NR, WDATA / colb));
+        const uint8_t *ubase = (S.dense ? a.D : a.U[S.tag]) + S.src;
+        const uint8_t *zbase = reinterpret_cast<const uint8_t *>(a.v + S.vbeg * NR);
+        for (int c0 = 0; c0 < S.ncols; c0 += cs, ++n) {
+          const int c1 = min(S.ncols, c0 + cs);
+          const int s = n % G::STAGES;
+          if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
+          uint8_t *st = smem + s * G::STAGE;
+          const uint8_t *usrc = ubase + (int64_t)c0 * colb;
+          const int64_t ulen = (int64_t)(c1 - c0) * colb;
+          const uint8_t *zsrc = zbase + (int64_t)c0 * NR * 8;
+          const int64_t zlen = (int64_t)(c1 - c0) * NR * 8;
+          Meta *m = reinterpret_cast<Meta *>(st + WBUF + G::XBUF);
+          m->kind = 0;
+          m->wlead = (int)((uintptr_t)usrc & 15);
+          m->xlead = (int)((uintptr_t)zsrc & 15);
+          m->r0 = c0;
+          m->r1 = c1;
+          m->flags = (si + 1 == Lf.s1 && c1 == S.ncols) ? 1 : 0;
+          m->a = Lf.nr;
+          m->b = S.tag | (S.dense << 8);
+          m->p = Lf.r0;
+          mbar_expect_tx(&full[s], window_bytes(usrc, ulen) + window_bytes(zsrc, zlen));
+          uint32_t tx = 0;
+          stage_copy(st, usrc, ulen, &full[s], pol_w, tx);
+          stage_copy(st + WBUF, zsrc, zlen, &full[s], pol_x, tx);
         }
       }
+      li = nxt;
     }
+    const int s = n % G::STAGES;
+    if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
+    reinterpret_cast<Meta *>(smem + s * G::STAGE + WBUF + G::XBUF)->kind = 1;
+    mbar_arrive(&full[s]);
     return;
   }
-  const int tid = threadIdx.x;  // 0 .. NCW*32-1
-  int n = 0;
-  for (int64_t li = blockIdx.x; li < a.nleaves; li += gridDim.x) {
-    const P2Leaf Lf = a.leaves[li];
-    const int nr = Lf.nr;
-    const int G = (NCW * 32) / nr;  // nr <= 256 (leaf_size limit)
+  // --------------------------------------------------------------------- consumers
+  const int tid = threadIdx.x;
+  double acc[NR];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) acc[k] = 0.0;
+  for (int n = 0;; ++n) {
+    const int s = n % G::STAGES;
+    mbar_wait(&full[s], (n / G::STAGES) & 1);
+    const uint8_t *st = smem + s * G::STAGE;
+    const Meta m = *reinterpret_cast<const Meta *>(st + WBUF + G::XBUF);
+    if (m.kind) break;
+    const int nr = m.a;
+    const int Gn = NCT / nr;  // nr <= 256 (leaf_size limit)
     const int rr = tid % nr, g = tid / nr;
-    const bool active = g < G;
-    double acc[NR];
-#pragma unroll
-    for (int q = 0; q < NR; ++q) acc[q] = 0.0;
-    for (int64_t ci = Lf.c0; ci < Lf.c1; ++ci, ++n) {
-      const int s = n % STAGES;
-      const P2Chunk C = a.chunks[ci];
-      mbar_wait(&full[s], (n / STAGES) & 1);
-      const uint8_t *stage = smem + s * STAGE_BYTES;
-      if (active) {
-        switch (C.tag) {
-          case TAG_FP64: p2_chunk<TAG_FP64, NR>(stage, C, nr, rr, g, G, a.v, acc); break;
-          case TAG_FP32: p2_chunk<TAG_FP32, NR>(stage, C, nr, rr, g, G, a.v, acc); break;
-          case TAG_FP16: p2_chunk<TAG_FP16, NR>(stage, C, nr, rr, g, G, a.v, acc); break;
-          default: p2_chunk<TAG_BF16, NR>(stage, C, nr, rr, g, G, a.v, acc); break;
-        }
+    if (g < Gn) {
+      const uint8_t *ust = st + m.wlead;
+      const double *zst = reinterpret_cast<const double *>(st + WBUF + m.xlead);
+      const int ncols = m.r1 - m.r0;
+      switch (m.b & 0xff) {
+        case TAG_FP64: p2_cols<TAG_FP64, NR>(ust, zst, ncols, nr, rr, g, Gn, acc); break;
+        case TAG_FP32: p2_cols<TAG_FP32, NR>(ust, zst, ncols, nr, rr, g, Gn, acc); break;
+        case TAG_FP16: p2_cols<TAG_FP16, NR>(ust, zst, ncols, nr, rr, g, Gn, acc); break;
+        default: p2_cols<TAG_BF16, NR>(ust, zst, ncols, nr, rr, g, Gn, acc); break;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // fixed-order reduction over column groups, then scatter y[perm[t]] (a10)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (m.flags & 1) {  // last stage of the leaf: fixed-order reduction over groups, scatter (a10)
 #pragma unroll
-    for (int q = 0; q < NR; ++q) red[tid * NR + q] = acc[q];
-    consumer_sync();
-    if (tid < nr) {
-      double s[NR];
+      for (int k = 0; k < NR; ++k) red[tid * NR + k] = acc[k];
+      consumer_sync();
+      if (tid < nr) {
+        double sum[NR];
 #pragma unroll
-      for (int q = 0; q < NR; ++q) s[q] = 0.0;
-      for (int gg = 0; gg < G; ++gg)
+        for (int k = 0; k < NR; ++k) sum[k] = 0.0;
+        for (int gg = 0; gg < Gn; ++gg)
 #pragma unroll
-        for (int q = 0; q < NR; ++q) s[q] += red[(gg * nr + tid) * NR + q];
-      const int64_t i = a.perm[Lf.r0 + tid];
+          for (int k = 0; k < NR; ++k) sum[k] += red[(gg * nr + tid) * NR + k];
+        const int64_t i = a.perm[m.p + tid];
 #pragma unroll
-      for (int q = 0; q < NR; ++q) a.y[i + q * a.ldy] = s[q];
+        for (int k = 0; k < NR; ++k) a.y[i + k * a.ldy] = sum[k];
+      }
+      consumer_sync();
+#pragma unroll
+      for (int k = 0; k < NR; ++k) acc[k] = 0.0;
     }
-    consumer_sync();
   }
 }
 
 }  // namespace mv
 
-size_t p1_smem() { return mv::STAGES * mv::STAGE_BYTES + 2 * mv::STAGES * sizeof(uint64_t); }
-size_t p2_smem(int nr) {
-  return mv::STAGES * mv::STAGE_BYTES + 2 * mv::STAGES * sizeof(uint64_t) + sizeof(double) * mv::NCW * 32 * nr;
-}
-
 template <int NR>
 void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
   using namespace mv;
+  using G = Geo<NR>;
   int dev = 0, nsm = 148;
   HH_CUDA(cudaGetDevice(&dev));
   HH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   double *v = H->v.as<double>();
+  int *ctr = H->ctr.as<int>();
   cudaEvent_t ev[4];
   auto mark = [&](int i) {
     if (!H->prof) return;
@@ -310,21 +421,21 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     H->prof_ev.push_back(ev[i]);
   };
   mark(0);
-  // a7 gather
-  k_gather<NR><<<nsm * 8, 256, 0, st>>>(H->d_perm.as<int32_t>(), x + (int64_t)col0 * H->N, H->N, H->N, v);
+  // a7 gather (+ counter reset)
+  k_gather<NR><<<nsm * 8, 256, 0, st>>>(H->d_perm.as<int32_t>(), x + (int64_t)col0 * H->N, H->N, H->N, v, ctr);
   HH_LAUNCHED();
   mark(1);
   // a8 phase 1
-  if (H->n_p1_items > 0) {
+  if (H->n_p1_tiles > 0) {
     P1Args a{};
-    a.items = H->p1_items.as<P1Item>();
-    a.entries = H->p1_entries.as<P1Entry>();
-    a.nitems = H->n_p1_items;
+    a.tiles = H->p1_tiles.as<P1Tile>();
+    a.zmap = H->zmap.as<int32_t>();
+    a.ntiles = H->n_p1_tiles;
     for (int g = 0; g < 4; ++g) a.W[g] = H->W[g].as<uint8_t>();
     a.v = v;
-    a.partial = H->partial.as<double>();
     a.N = H->N;
-    const size_t sm = p1_smem();
+    a.ctr = ctr;
+    const size_t sm = G::smem(false);
     static bool attr1[17] = {};
     if (!attr1[NR]) {
       HH_CUDA(cudaFuncSetAttribute(k_phase1<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -332,19 +443,15 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     }
     int per_sm = 0;
     HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phase1<NR>, THREADS, sm));
-    const int64_t grid = std::min<int64_t>(H->n_p1_items, (int64_t)nsm * std::max(1, per_sm));
+    const int64_t grid = std::min<int64_t>(H->n_p1_tiles, (int64_t)nsm * std::max(1, per_sm));
     k_phase1<NR><<<(unsigned)grid, THREADS, sm, st>>>(a);
     HH_LAUNCHED();
-    if (H->n_combines > 0) {
-      k_combine<NR><<<nsm * 4, 256, 0, st>>>(H->combines.as<Combine>(), H->n_combines, H->partial.as<double>(), v, H->N);
-      HH_LAUNCHED();
-    }
   }
   mark(2);
   // a9 + a10 phase 2 with fused scatter
   P2Args b{};
   b.leaves = H->p2_leaves.as<P2Leaf>();
-  b.chunks = H->p2_chunks.as<P2Chunk>();
+  b.segs = H->p2_segs.as<P2Seg>();
   b.nleaves = H->n_p2_leaves;
   for (int g = 0; g < 4; ++g) b.U[g] = H->U[g].as<uint8_t>();
   b.D = H->D.as<uint8_t>();
@@ -352,7 +459,8 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   b.perm = H->d_perm.as<int32_t>();
   b.y = y + (int64_t)col0 * H->N;
   b.ldy = H->N;
-  const size_t sm2 = p2_smem(NR);
+  b.ctr = ctr;
+  const size_t sm2 = G::smem(true);
   static bool attr2[17] = {};
   if (!attr2[NR]) {
     HH_CUDA(cudaFuncSetAttribute(k_phase2<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));

@@ -56,11 +56,11 @@ class hh_info_t(C.Structure):
 
 
 BLOCK_DTYPE = np.dtype([
-    ("tgt", "<i8"), ("src", "<i8"), ("zoff", "<i8"), ("w_off", "<i8"), ("ucol", "<i8"), ("d_off", "<i8"),
+    ("tgt", "<i8"), ("src", "<i8"), ("zoff", "<i8"), ("w_off", "<i8"), ("wcol", "<i8"), ("ucol", "<i8"), ("d_off", "<i8"),
     ("nb2", "<f8"), ("tot", "<f8"), ("maxabs", "<f8"), ("rank", "<i4"),
     ("level", "u1"), ("kind", "u1"), ("tag", "u1"), ("storage", "u1"),
 ])
-assert BLOCK_DTYPE.itemsize == 80
+assert BLOCK_DTYPE.itemsize == 88
 
 
 class hh_export_t(C.Structure):

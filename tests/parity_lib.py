@@ -53,6 +53,7 @@ def check_packing(ex):
     np.testing.assert_array_equal(lay["zoff"][lr], B["zoff"][lr], err_msg="zoff")
     has = lr & (B["rank"] > 0)
     np.testing.assert_array_equal(lay["w_off"][has], B["w_off"][has], err_msg="w_off")
+    np.testing.assert_array_equal(lay["wcol"][has], B["wcol"][has], err_msg="wcol")
     np.testing.assert_array_equal(lay["ucol"][has], B["ucol"][has], err_msg="ucol")
     dn = ~lr
     np.testing.assert_array_equal(lay["d_off"][dn], B["d_off"][dn], err_msg="d_off")

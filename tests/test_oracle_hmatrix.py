@@ -238,7 +238,11 @@ def test_pack_roundtrip_and_invariants(tiny_oracle):
         if p == 0:
             continue
         assert lay["w_off"][b] % 16 == 0
-        put(("W", g), int(lay["w_off"][b]), Wf.T.ravel(), g)
+        offs = PK.w_offsets(lay, b, g)                      # (n, p) element offsets
+        bits = np.frombuffer(F.to_storage_bits(Wf.ravel(), g).tobytes(), np.uint8).reshape(-1, F.BYTES[g])
+        for k in range(F.BYTES[g]):
+            arenas[("W", g)][offs.ravel() + k] = bits[:, k]
+            used[("W", g)][offs.ravel() + k] += 1
         l = int(part.level[b])
         s = tr.d * (tr.L - l)
         for R in range(int(part.tgt[b]) << s, (int(part.tgt[b]) + 1) << s):
@@ -246,6 +250,7 @@ def test_pack_roundtrip_and_invariants(tiny_oracle):
             if r1 > r0:
                 off = int(lay["u_leaf_off"][g, R]) + int(lay["ucol"][b]) * (r1 - r0) * F.BYTES[g]
                 put(("U", g), off, U[r0 - i0:r1 - i0].T.ravel(), g)
+    assert np.any(lay["wpanel"] > PK.CT)  # multi-tile W panels are exercised
     for k in used:                      # no byte written twice
         assert used[k].max(initial=0) <= 1
     for g in range(4):
