@@ -1,4 +1,5 @@
 """Pins for oracle/tree.py and oracle/partition.py.  CPU only."""
+import os
 from fractions import Fraction
 
 import numpy as np
@@ -184,22 +185,29 @@ def test_special_cases():
     assert set(np.unique(hh.kind)) <= {PT.FAR, PT.NBR, PT.SIB, PT.DIAG}
 
 
-# Golden counts: cell-centre grids (one point per leaf), derived
-# independently there by closed-form offset counting.
-GOLDEN = [
-    (2, 4, 1.0, PT.SWITCH_NONE, {(2, PT.FAR): 76, (3, PT.FAR): 1868, (4, PT.FAR): 11500, (4, PT.LNBR): 4436}),
-    (2, 4, 1.0, 0, {(1, PT.SIB): 12, (2, PT.SIB): 48, (3, PT.SIB): 192, (4, PT.SIB): 768}),
-    (2, 4, 1.0, 1, {(1, PT.NBR): 12, (2, PT.SIB): 48, (3, PT.SIB): 192, (4, PT.SIB): 768}),
-    (2, 4, 1.0, 2, {(2, PT.FAR): 76, (2, PT.NBR): 164, (3, PT.SIB): 192, (4, PT.SIB): 768}),
-    (2, 4, 1.0, 3, {(2, PT.FAR): 76, (3, PT.FAR): 1868, (3, PT.NBR): 948, (4, PT.SIB): 768}),
-    (2, 4, 1.0, 4, {(2, PT.FAR): 76, (3, PT.FAR): 1868, (4, PT.FAR): 11500, (4, PT.NBR): 4436}),
-    (2, 4, np.sqrt(2), PT.SWITCH_NONE, {(2, PT.FAR): 156, (3, PT.FAR): 1116, (4, PT.FAR): 5628, (4, PT.LNBR): 1860}),
-    (2, 4, np.sqrt(2), 3, {(2, PT.FAR): 156, (3, PT.FAR): 1116, (3, PT.NBR): 420, (4, PT.SIB): 768}),
-    (3, 3, 1.0, PT.SWITCH_NONE, {(2, PT.FAR): 1416, (3, PT.FAR): 133944, (3, PT.LNBR): 37064}),
-    (3, 3, 1.0, 2, {(2, PT.FAR): 1416, (2, PT.NBR): 2616, (3, PT.SIB): 3584}),
-    (3, 3, np.sqrt(3), PT.SWITCH_NONE, {(2, PT.FAR): 3096, (3, PT.FAR): 53352, (3, PT.LNBR): 10136}),
-    (3, 3, np.sqrt(3), 3, {(2, PT.FAR): 3096, (3, PT.FAR): 53352, (3, PT.NBR): 10136}),
-]
+# Golden counts: cell-centre grids (one point per leaf), tests/golden/partition_counts.txt
+# (derived there by closed-form offset counting, Appendix A.1).
+def _load_golden():
+    kinds = {"F": PT.FAR, "N": PT.NBR, "S": PT.SIB, "D": PT.LNBR}
+    etas = {"1": 1.0, "sqrt2": np.sqrt(2.0), "sqrt3": np.sqrt(3.0)}
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "partition_counts.txt")
+    rows = []
+    for line in open(path):
+        line = line.split("#", 1)[0].split()
+        if not line:
+            continue
+        d, L, eta, s = int(line[0]), int(line[1]), etas[line[2]], line[3]
+        s = PT.SWITCH_NONE if s == "none" else int(s)
+        counts = {}
+        for tok in line[4:]:
+            lv, kc = tok.split(":")
+            counts[(int(lv[1:]), kinds[kc[0]])] = int(kc[1:])
+        rows.append((d, L, eta, s, counts))
+    return rows
+
+
+GOLDEN = _load_golden()
+assert len(GOLDEN) == 17
 
 
 @pytest.mark.parametrize("d,L,eta,s,counts", GOLDEN)
