@@ -2,6 +2,8 @@
 
     python -m paper_2604_09147_b200.build            # incremental
     python -m paper_2604_09147_b200.build --force
+    python -m paper_2604_09147_b200.build --variant NAME -DHH_MV_CVT=1 ...   # side-by-side
+      experiment build -> libhh_NAME.so (load it with HH_LIB=<path>); not the product build
 """
 from __future__ import annotations
 
@@ -30,12 +32,12 @@ def _stale(src, obj):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(name, force, verbose_ptxas):
+def _compile(name, force, verbose_ptxas, objdir=OBJ, defines=()):
     src = os.path.join(CSRC, name)
-    obj = os.path.join(OBJ, name + ".o")
+    obj = os.path.join(objdir, name + ".o")
     if not force and not _stale(src, obj):
         return obj, ""
-    cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *FLAGS, *defines, "-c", src, "-o", obj]
     if verbose_ptxas and name.endswith(".cu"):
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -44,22 +46,28 @@ def _compile(name, force, verbose_ptxas):
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose_ptxas: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose_ptxas: bool = False, variant: str | None = None, defines=()) -> str:
+    objdir, lib = OBJ, LIB
+    if variant:
+        objdir = os.path.join(OBJ, "variant_" + variant)
+        lib = os.path.join(HERE, f"libhh_{variant}.so")
+    os.makedirs(objdir, exist_ok=True)
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        outs = list(ex.map(lambda s: _compile(s, force, verbose_ptxas), SOURCES))
+        outs = list(ex.map(lambda s: _compile(s, force, verbose_ptxas, objdir, defines), SOURCES))
     objs = [o for o, _ in outs]
     if verbose_ptxas:
         for _, log in outs:
             if log:
                 print(log, file=sys.stderr)
-    if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs, "-lcudart"]
+    if force or not os.path.exists(lib) or any(os.path.getmtime(o) > os.path.getmtime(lib) for o in objs):
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv))
+    var = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else None
+    defs = [a for a in sys.argv if a.startswith("-D")]
+    print(build(force="--force" in sys.argv or bool(var), verbose_ptxas="-v" in sys.argv, variant=var, defines=defs))

@@ -203,8 +203,10 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
         if (H->storage[b] == STORE_LR && H->rank[b] > 0) jobs.push_back(CompressJob{(int64_t)b, H->kfinal[b]});
       std::vector<CompressResult> res;
       run_compress(H, pts.as<double>(), jobs, true, &ar, res, st, workspace_budget());
+      // pass 2 writes the factors of the pass-1 rank; its maxabs must reproduce pass 1's
+      // (the range guard decided the tags from it): a cheap determinism check
       int64_t mism = 0;
-      for (size_t i = 0; i < jobs.size(); ++i) mism += res[i].p != H->rank[jobs[i].block];
+      for (size_t i = 0; i < jobs.size(); ++i) mism += res[i].maxabs != H->maxabs[jobs[i].block];
       HH_REQUIRE(mism == 0, HH_ECUDA, "pass-2 recompression disagreed with pass 1 (non-deterministic kernel)");
       // dense blocks (diagonal + dense neighbours) after tagging
       std::vector<int64_t> dn2;

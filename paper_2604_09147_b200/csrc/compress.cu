@@ -667,7 +667,8 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
       off = c.otau + 2 * c.k + 8;
       c.gid = b;
       c.task0 = 0;
-      if (write) {
+      if (write) {  // pass 2: rank known from pass 1 (bitwise-identical pipeline)
+        c.pfound = H->rank[b];
         c.tag = H->tag[b];
         c.w_off = H->w_off[b];
         c.ucol = H->ucol[b];
@@ -731,11 +732,15 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
     k_jacobi<<<nb, JT, jsmem, st>>>(db, ws);
     HH_LAUNCHED();
     mark(5);
-    k_resid<<<(unsigned)tR.size(), THREADS, 0, st>>>(dR, db, ws, pts, H->N, H->d, K, partb.as<double>());
-    HH_LAUNCHED();
-    mark(6);
-    k_decide<<<(nb + 127) / 128, 128, 0, st>>>(db, nb, ws, partb.as<double>(), H->eps, delta);
-    HH_LAUNCHED();
+    if (!write) {  // pass 2 knows the rank: no residual / decision needed
+      k_resid<<<(unsigned)tR.size(), THREADS, 0, st>>>(dR, db, ws, pts, H->N, H->d, K, partb.as<double>());
+      HH_LAUNCHED();
+      mark(6);
+      k_decide<<<(nb + 127) / 128, 128, 0, st>>>(db, nb, ws, partb.as<double>(), H->eps, delta);
+      HH_LAUNCHED();
+    } else {
+      mark(6);
+    }
     mark(7);
     Arenas a{};
     if (write) a = *ar;

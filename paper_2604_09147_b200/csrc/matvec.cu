@@ -39,7 +39,11 @@ template <int NR> struct Geo {
   static constexpr int XELEMS = XDATA / 8;                // doubles (rows x NR)
   static constexpr int XBUF = XDATA + 32;
   static constexpr int STAGE = WBUF + XBUF + META;
+#ifdef HH_MV_STAGES
+  static constexpr int STAGES = HH_MV_STAGES;
+#else
   static constexpr int STAGES = NR == 2 ? 5 : 6;
+#endif
   static constexpr size_t smem(bool red) {
     return (size_t)STAGES * STAGE + 2 * STAGES * sizeof(uint64_t) + (red ? sizeof(double) * NCT * NR : 0);
   }
@@ -112,12 +116,44 @@ __device__ __forceinline__ uint32_t window_bytes(const uint8_t *src, int64_t byt
   return bytes > 0 ? (uint32_t)(((s + bytes + 15) & ~(uintptr_t)15) - (s & ~(uintptr_t)15)) : 0u;
 }
 
+template <int TAG> struct Elem;
+template <> struct Elem<TAG_FP64> { using T = double; };
+template <> struct Elem<TAG_FP32> { using T = float; };
+template <> struct Elem<TAG_FP16> { using T = __half; };
+template <> struct Elem<TAG_BF16> { using T = uint16_t; };
+
+// Tunables (compile-time; scripts/variants.sh builds alternatives side by side).
+#ifndef HH_MV_CHAINS
+#define HH_MV_CHAINS 4   // independent fp64 accumulation chains per thread at NR = 1
+#endif
+#ifndef HH_MV_CVT
+#define HH_MV_CVT 0      // 0: F2F conversion; 1: bit placement + exact power-of-two DMUL
+#endif
+
+// exact up-conversion of a stored element to fp64
 template <int TAG>
-__device__ __forceinline__ double ld_up(const uint8_t *base, int i) {
-  if (TAG == TAG_FP64) return reinterpret_cast<const double *>(base)[i];
-  if (TAG == TAG_FP32) return (double)reinterpret_cast<const float *>(base)[i];
-  if (TAG == TAG_FP16) return (double)__half2float(reinterpret_cast<const __half *>(base)[i]);
-  return (double)__uint_as_float(((uint32_t) reinterpret_cast<const uint16_t *>(base)[i]) << 16);
+__device__ __forceinline__ double up(const typename Elem<TAG>::T v) {
+  if constexpr (TAG == TAG_FP64) {
+    return v;
+  } else if constexpr (HH_MV_CVT == 1) {
+    // place sign / exponent / mantissa bits in an fp64 with the same (unbiased-shifted)
+    // exponent field, then rescale by the exact power of two between the two biases
+    // (normals, subnormals and zeros are all exact; factors are finite by construction)
+    if constexpr (TAG == TAG_FP32) {
+      const uint32_t b = __float_as_uint(v);
+      return __hiloint2double((int)((b & 0x80000000u) | ((b & 0x7FFFFFFFu) >> 3)), (int)(b << 29)) * 0x1p896;
+    } else if constexpr (TAG == TAG_FP16) {
+      const uint32_t h = __half_as_ushort(v);
+      return __hiloint2double((int)(((h & 0x8000u) << 16) | ((h & 0x7FFFu) << 10)), 0) * 0x1p1008;
+    } else {
+      const uint32_t h = v;
+      return __hiloint2double((int)(((h & 0x8000u) << 16) | ((h & 0x7FFFu) << 13)), 0) * 0x1p896;
+    }
+  } else {
+    if constexpr (TAG == TAG_FP32) return (double)v;
+    else if constexpr (TAG == TAG_FP16) return (double)__half2float(v);
+    else return (double)__uint_as_float(((uint32_t)v) << 16);
+  }
 }
 
 // --------------------------------------------------------------------------- gather
@@ -143,19 +179,53 @@ struct P1Args {
   int *ctr;
 };
 
+// Independent accumulation chains per thread: enough to cover the fp64 FMA latency with
+// the few warps per scheduler a 2-CTA/SM persistent kernel has.
+template <int NR> constexpr int chains() { return NR >= HH_MV_CHAINS ? 1 : HH_MV_CHAINS / NR; }
+
+// Generic strided dot-accumulate: acc[k] += sum_j up(e[j * es]) * v[j * vs + k] for the j
+// this thread owns (j = 0 .. cnt-1), with CH interleaved partial sums merged in fixed order.
+template <int TAG, int NR>
+__device__ __forceinline__ void strided_acc(const typename Elem<TAG>::T *e, const double *v, int cnt, int es,
+                                            int vs, double (&acc)[NR]) {
+  constexpr int CH = chains<NR>();
+  double part[CH][NR];
+#pragma unroll
+  for (int h = 0; h < CH; ++h)
+#pragma unroll
+    for (int k = 0; k < NR; ++k) part[h][k] = 0.0;
+  int j = 0;
+  for (; j + CH <= cnt; j += CH) {
+    double a[CH];
+#pragma unroll
+    for (int h = 0; h < CH; ++h) a[h] = up<TAG>(e[h * es]);
+#pragma unroll
+    for (int h = 0; h < CH; ++h)
+#pragma unroll
+      for (int k = 0; k < NR; ++k) part[h][k] = __fma_rn(a[h], v[h * vs + k], part[h][k]);
+    e += CH * es;
+    v += CH * vs;
+  }
+  for (; j < cnt; ++j) {
+    const double a0 = up<TAG>(e[0]);
+#pragma unroll
+    for (int k = 0; k < NR; ++k) part[0][k] = __fma_rn(a0, v[k], part[0][k]);
+    e += es;
+    v += vs;
+  }
+#pragma unroll
+  for (int h = 0; h < CH; ++h)
+#pragma unroll
+    for (int k = 0; k < NR; ++k) acc[k] += part[h][k];
+}
+
 // rows [0, nrows) of the staged window; thread (c, q) takes rows q, q + Q, ...
 template <int TAG, int NR>
 __device__ __forceinline__ void p1_rows(const uint8_t *wst, const double *xst, int nrows, int ct, int c, int q,
                                         int Q, double (&acc)[NR]) {
-  constexpr int w = TAG == TAG_FP64 ? 8 : (TAG == TAG_FP32 ? 4 : 2);
-  const uint8_t *col = wst + c * w;
-  const int stride = ct;
-#pragma unroll 4
-  for (int i = q; i < nrows; i += Q) {
-    const double a = ld_up<TAG>(col, i * stride);
-#pragma unroll
-    for (int k = 0; k < NR; ++k) acc[k] = __fma_rn(a, xst[i * NR + k], acc[k]);
-  }
+  using T = typename Elem<TAG>::T;
+  const int cnt = q < nrows ? (nrows - q + Q - 1) / Q : 0;
+  strided_acc<TAG, NR>(reinterpret_cast<const T *>(wst) + q * ct + c, xst + q * NR, cnt, Q * ct, Q * NR, acc);
 }
 
 template <int NR>
@@ -281,12 +351,9 @@ struct P2Args {
 template <int TAG, int NR>
 __device__ __forceinline__ void p2_cols(const uint8_t *ust, const double *zst, int ncols, int nr, int rr, int g, int G,
                                         double (&acc)[NR]) {
-#pragma unroll 4
-  for (int c = g; c < ncols; c += G) {
-    const double u = ld_up<TAG>(ust, c * nr + rr);
-#pragma unroll
-    for (int k = 0; k < NR; ++k) acc[k] = __fma_rn(u, zst[c * NR + k], acc[k]);
-  }
+  using T = typename Elem<TAG>::T;
+  const int cnt = g < ncols ? (ncols - g + G - 1) / G : 0;
+  strided_acc<TAG, NR>(reinterpret_cast<const T *>(ust) + g * nr + rr, zst + g * NR, cnt, G * nr, G * NR, acc);
 }
 
 template <int NR>

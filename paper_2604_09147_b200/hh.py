@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhh.so")
+LIB_PATH = os.environ.get("HH_LIB") or os.path.join(_HERE, "libhh.so")   # HH_LIB: experiment builds
 
 HH_OK, HH_EINVAL, HH_ENOMEM, HH_ECUDA, HH_ENUMERIC, HH_EDEPTH, HH_EUNSUPPORTED = range(7)
 K_LOG, K_INV_R, K_INV_R2, K_GAUSS, K_EXP = range(5)

@@ -1,0 +1,168 @@
+"""GPU parity at the BASELINE.json full sizes, in the launch configuration bench.py times
+(hh_build + hh_matvec through the C-ABI, nrhs = 1 and the config's multi-RHS case).
+
+At these sizes the oracle cannot rebuild everything, so each check runs on what it can
+afford, one by one:
+  (1a) perm, leaf offsets and the whole block table — the oracle's own tree and partition
+       of the full point set (cheap at every size), bit-exact;
+  (1c) the oracle's packing function on the GPU's (rank, tag, storage) — every offset;
+  (1b) ranks / ||H~_b||^2 / ||H_b||^2 of a stratified sample of blocks against the oracle's
+       LAPACK truncated SVD of the same block; tags by Eq. 4.4 on the oracle's nb2 with the
+       exported ||H~||^2 (itself checked to be the fixed-order Alg. 4 sum of the table);
+  (2)  complete output rows of sampled leaves: the oracle's Alg. 3 over every block whose
+       target contains the leaf, on factors decoded from ranged arena exports, <= 1e-12;
+  (3)  e_mv estimated from sampled rows of the dense product (||A||_F^2 estimated from the
+       same rows) <= 10 eps.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import compress as OC
+from oracle import dense as D
+from oracle import formats as F
+from oracle import hmatrix as HM
+from oracle import kernels as OK
+from oracle import pack as PK
+from oracle import partition as PT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import parity_lib as PL  # noqa: E402
+from paper_2604_09147_b200 import hh  # noqa: E402
+
+FULL = ["2d_medium", "3d_laplace", "3d_large"]
+
+
+@pytest.fixture(scope="module", params=FULL)
+def full(request):
+    name = request.param
+    cfg = W.CONFIGS[name]
+    P = W.make_points(cfg)
+    H = PL.gpu_build(P, cfg)
+    ex = PL.export(H, arenas=False)
+    tr, part = PL.oracle_partition(P, cfg)
+    B = ex["blocks"]
+    lay = PK.pack(ex["leaf_start"], tr.d, tr.L, B["level"], B["tgt"], B["src"], B["rank"], B["tag"], B["storage"])
+    yield name, cfg, P, H, ex, tr, part, lay
+    hh.hh_free(H)
+
+
+def test_full_1a_partition(full):
+    name, cfg, P, H, ex, tr, part, lay = full
+    np.testing.assert_array_equal(ex["perm"].astype(np.int64), tr.perm)
+    np.testing.assert_array_equal(ex["leaf_start"], tr.leaf_start)
+    B = ex["blocks"]
+    assert B.size == len(part)
+    for f, ref in (("level", part.level), ("kind", part.kind), ("tgt", part.tgt), ("src", part.src)):
+        np.testing.assert_array_equal(B[f].astype(np.int64), ref, err_msg=f)
+
+
+def test_full_1c_packing(full):
+    PL.check_packing(full[4])
+
+
+def test_full_1b_sampled_blocks(full):
+    name, cfg, P, H, ex, tr, part, lay = full
+    B = ex["blocks"]
+    info = ex["info"]
+    # Alg. 4 consistency of the exported norm (fixed-order sum of the table's own entries)
+    lr = B["storage"] == 0
+    s = float(np.sum(B["nb2"][lr])) + float(np.sum(B["tot"][~lr]))
+    assert abs(s - info["norm2"]) <= 1e-12 * info["norm2"]
+    rng = np.random.default_rng(77)
+    m, n = lay["m"], lay["n"]
+    nbad, checked = 0, 0
+    for l in np.unique(B["level"]):
+        for k in np.unique(B["kind"]):
+            sel = np.nonzero(lr & (B["level"] == l) & (B["kind"] == k) & (np.maximum(m, n) <= 2048))[0]
+            if sel.size == 0:
+                continue
+            for b in rng.choice(sel, size=min(12, sel.size), replace=False):
+                i0, j0 = int(lay["i0"][b]), int(lay["j0"][b])
+                A, _ = OK.block(P, tr.perm[i0:i0 + m[b]], tr.perm[j0:j0 + n[b]], cfg["kernel"], cfg["scale"])
+                c = OC.lr_compress(A, cfg["eps"])
+                checked += 1
+                assert abs(B["tot"][b] - c["tot"]) <= 1e-12 * c["tot"], (b, B["tot"][b], c["tot"])
+                if B["rank"][b] != c["p"]:
+                    assert c["margin"] < 1e-6, (b, B["rank"][b], c["p"], c["margin"])
+                    nbad += 1
+                    continue
+                assert abs(B["nb2"][b] - c["nb2"]) <= 2e-10 * c["nb2"] + 1e-300
+                tag, _ = HM.choose_tag(c["nb2"], info["norm2"], cfg["eps"], tr.d, int(l), cfg["pset"])
+                if tag != B["tag"][b]:
+                    # only when the Eq. 4.4 decision sits on the threshold
+                    u = max(F.unit_roundoff(int(B["tag"][b])), F.unit_roundoff(tag))
+                    lhs = u * u * 2.0 ** (tr.d * int(l)) * c["nb2"]
+                    assert abs(lhs - cfg["eps"] ** 2 * info["norm2"]) <= 1e-9 * lhs
+    assert checked > 20 and nbad <= max(1, checked // 200)
+
+
+def _leaf_blocks(B, lay, tr, R):
+    """Blocks whose target cluster contains leaf R (every level), in canonical order."""
+    d, L = tr.d, tr.L
+    lv = B["level"].astype(np.int64)
+    return np.nonzero((B["tgt"] == (np.int64(R) >> (d * (L - lv)))) & ((B["storage"] == 1) | (B["rank"] > 0)))[0]
+
+
+def _oracle_leaf_rows(H, B, lay, tr, R, xt):
+    """Alg. 3 restricted to the rows of leaf R, on factors decoded with the oracle's packing
+    function from ranged arena exports.  xt: x in tree order (N, nrhs)."""
+    r0, r1 = int(tr.leaf_start[R]), int(tr.leaf_start[R + 1])
+    nr = r1 - r0
+    y = np.zeros((nr, xt.shape[1]))
+    for b in _leaf_blocks(B, lay, tr, R):
+        j0, nn = int(lay["j0"][b]), int(lay["n"][b])
+        if B["storage"][b] == 1:                       # dense (fp64)
+            i0, mm = int(lay["i0"][b]), int(lay["m"][b])
+            off = int(lay["d_off"][b])
+            raw = hh.export_arena(H, hh.ARENA_D, off, mm * nn * 8)
+            Dm = F.from_storage_bytes(raw, F.FP64).reshape(nn, mm).T
+            y += Dm[r0 - i0:r1 - i0] @ xt[j0:j0 + nn]
+            continue
+        g, p = int(B["tag"][b]), int(B["rank"][b])
+        w = F.BYTES[g]
+        offs = PK.w_offsets(lay, b, g)
+        lo, hi = int(offs.min()), int(offs.max()) + w
+        raw = hh.export_arena(H, hh.ARENA_W + g, lo, hi - lo)
+        elem = np.stack([raw[offs - lo + k] for k in range(w)], axis=-1).reshape(-1)
+        Wb = F.from_storage_bytes(elem, g).reshape(nn, p)
+        base = int(lay["u_leaf_off"][g, R]) + int(lay["ucol"][b]) * nr * w
+        Ub = F.from_storage_bytes(hh.export_arena(H, hh.ARENA_U + g, base, nr * p * w), g).reshape(p, nr).T
+        y += Ub @ (Wb.T @ xt[j0:j0 + nn])
+    return y
+
+
+def test_full_check2_sampled_leaves(full):
+    name, cfg, P, H, ex, tr, part, lay = full
+    B = ex["blocks"]
+    rng = np.random.default_rng(5)
+    nonempty = np.nonzero(np.diff(tr.leaf_start) > 0)[0]
+    leaves = rng.choice(nonempty, size=2, replace=False)
+    for nrhs in sorted({1, cfg["nrhs"], 16 if name == "3d_large" else 1}):
+        x = W.make_rhs(cfg, nrhs)
+        y = PL.gpu_matvec(H, x)
+        xt = x[tr.perm]
+        for R in leaves:
+            r0, r1 = int(tr.leaf_start[R]), int(tr.leaf_start[R + 1])
+            yo = _oracle_leaf_rows(H, B, lay, tr, int(R), xt)
+            yg = y[tr.perm[r0:r1]]
+            for c in range(nrhs):
+                assert PL.rel2(yg[:, c], yo[:, c]) <= 1e-12, (name, nrhs, R, c, PL.rel2(yg[:, c], yo[:, c]))
+
+
+def test_full_check3_sampled_rows(full):
+    name, cfg, P, H, ex, tr, part, lay = full
+    x = W.make_rhs(cfg, 1)
+    y = PL.gpu_matvec(H, x)
+    rng = np.random.default_rng(9)
+    N = cfg["N"]
+    rows = rng.choice(N, size=96, replace=False)
+    Ax, fro2_rows = D.dense_apply(P, cfg["kernel"], cfg["scale"], x, rows=rows, chunk=8)
+    r2 = float(np.sum((Ax[:, 0] - y[rows, 0]) ** 2))
+    e_est = np.sqrt(r2 * N / rows.size) / (np.sqrt(fro2_rows * N / rows.size) * np.linalg.norm(x))
+    assert e_est <= 10 * cfg["eps"], e_est

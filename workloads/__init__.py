@@ -85,6 +85,14 @@ SMALL_CONFIGS = {
 }
 
 
+# Iteration proxy for the 3D N=2^20 config (same kernel, eps, leaf occupancy ~32; 8x fewer
+# points so it builds in seconds).  Not a BASELINE config: used by scripts/profile_matvec.py.
+PROXY_CONFIGS = {
+    "3d_exp_proxy": dict(k=20, N=131072, d=3, kernel=K_EXP, scale=0.1, leaf=64, eta=1.0, s=3,
+                         eps=1e-6, pset=P_MIXED, nrhs=1, xdist="normal"),
+}
+
+
 def make_points(cfg: dict) -> np.ndarray:
     return points_uniform(cfg["N"], cfg["d"], 1000 + cfg["k"], cfg.get("lo", 0.0), cfg.get("hi", 1.0))
 
