@@ -90,6 +90,25 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ----------------------------------------------------------------------------- multi-rank plumbing
+def max_over_ranks(x: float, device=None) -> float:
+    """Max over ranks of a per-rank device time (replicas: the job ends with the slowest
+    rank); identity without an initialised process group.  Works on nccl (CUDA tensors) and
+    gloo (CPU tensors, tests/test_bench_multirank.py)."""
+    import torch
+    import torch.distributed as tdist
+    if not (tdist.is_available() and tdist.is_initialized()) or tdist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_gbps(stored_bytes: int, steps: int, world: int, max_ms: float) -> float:
+    """Whole-job throughput: every replica streams `stored_bytes` per step; time = slowest rank."""
+    return stored_bytes * steps * world / (max_ms / 1e3) / 1e9
+
+
 # ----------------------------------------------------------------------------- oracle arm
 def oracle_sample(cfg: dict, target_bytes: float, seed: int = 0):
     """A bounded sample of the workload for the CPU oracle: the oracle's own tree and
@@ -233,13 +252,9 @@ def run_ours(args, rank, world, local_rank):
     hh.hh_matvec_profile(H, False)
     phase_ms, nchunks = hh.hh_matvec_timing(H)
     clocks = clk.stop()
-    ms = sum(a.elapsed_time(b) for a, b in evs)
-    if dist:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs), dev)
     per_step = ms / args.steps
-    value = stored * args.steps * world / (ms / 1e3) / 1e9
+    value = job_gbps(stored, args.steps, world, ms)
     # e2e: host buffers through hh_matvec_host (H2D of x, matvec, D2H of y inside)
     e2e = None
     if not args.no_e2e:
@@ -261,11 +276,7 @@ def run_ours(args, rank, world, local_rank):
             assert st == 0
             torch.cuda.synchronize()
             ee.append(a.elapsed_time(b))
-        e_ms = sum(ee) / len(ee)
-        if dist:
-            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-            e_ms = float(t.item())
+        e_ms = max_over_ranks(sum(ee) / len(ee), dev)
         e2e = {"value": round(stored * world / (e_ms / 1e3) / 1e9, 2), "unit": "GB/s",
                "matvecs_per_s": round(world * 1e3 / e_ms, 3), "ms_per_step": round(e_ms, 4),
                "h2d_bytes_per_step": int(8 * cfg["N"] * nrhs), "d2h_bytes_per_step": int(8 * cfg["N"] * nrhs)}

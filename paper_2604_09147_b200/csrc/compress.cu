@@ -52,15 +52,21 @@ namespace {
 
 constexpr int THREADS = 256;
 
-__device__ __forceinline__ double hash_uniform(uint64_t gid, uint64_t j, uint64_t c) {
-  uint64_t z = gid * 0x9E3779B97F4A7C15ull ^ (j + 0x632BE59BD9B4E019ull) * 0xBF58476D1CE4E5B9ull ^
-               (c + 0x8CB92BA72F3D8DD7ull) * 0x94D049BB133111EBull;
-  z ^= z >> 30;
-  z *= 0xBF58476D1CE4E5B9ull;
-  z ^= z >> 27;
-  z *= 0x94D049BB133111EBull;
-  z ^= z >> 31;
-  return (double)(z >> 11) * 0x1.0p-52 - 1.0;  // uniform in [-1, 1)
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {  // "lowbias32" integer finaliser
+  x ^= x >> 16;
+  x *= 0x7FEB352Du;
+  x ^= x >> 15;
+  x *= 0x846CA68Bu;
+  x ^= x >> 16;
+  return x;
+}
+
+// Sketch matrix Omega(j, c) of block gid: a counter-based hash, uniform on [-1, 1) in steps of
+// 2^-31; pure function of (gid, j, c) so pass 2 reproduces pass 1 bit for bit.
+__device__ __forceinline__ double hash_uniform(uint64_t gid, uint32_t j, uint32_t c) {
+  uint32_t h = mix32((uint32_t)gid * 0x9E3779B1u ^ (uint32_t)(gid >> 32) * 0x85EBCA77u ^ j * 0xC2B2AE3Du);
+  h = mix32(h ^ (c + 0x27D4EB2Fu) * 0x165667B1u);
+  return (double)(int32_t)h * 0x1p-31;
 }
 
 __device__ __forceinline__ double entry(const KernelFn &K, const double *pts, int64_t N, int d, int64_t a, int64_t b) {
@@ -75,11 +81,13 @@ __device__ __forceinline__ double entry(const KernelFn &K, const double *pts, in
 // ---------------------------------------------------------------- fused entry GEMM
 // mode 0: Y[:, c] = sum_j A(i, j) Omega(j, c)   rows = target cluster, cols = source
 // mode 1: Z[:, c] = sum_i A(i, j) Q(i, c)       rows = source cluster, cols = target
-constexpr int GT_M = 64, GT_N = 64, GT_K = 16;
+constexpr int GT_M = 64, GT_K = 16;
 
-template <int MODE>
+// GT_N = sketch columns per CTA tile (32 or 64, chosen per batch from its widest sketch)
+template <int MODE, int GT_N>
 __global__ void __launch_bounds__(THREADS) k_gemm_gen(const Task *__restrict__ tasks, CBlk *blks, double *ws,
                                                       const double *__restrict__ pts, int64_t N, int d, KernelFn K) {
+  constexpr int TC = GT_N / 16;  // output columns per thread
   const Task T = tasks[blockIdx.x];
   const CBlk &B = blks[T.blk];
   const int rows = MODE == 0 ? B.m : B.n;
@@ -99,7 +107,7 @@ __global__ void __launch_bounds__(THREADS) k_gemm_gen(const Task *__restrict__ t
     int64_t row = T.r0 + r;
     rp[kk][r] = row < rows ? pts[kk * N + rbase + row] : 0.0;
   }
-  double acc[4][4] = {};
+  double acc[4][TC] = {};
   const double *X = ws + (MODE == 0 ? 0 : B.oq);
   for (int j0 = 0; j0 < cols; j0 += GT_K) {
     __syncthreads();
@@ -124,7 +132,7 @@ __global__ void __launch_bounds__(THREADS) k_gemm_gen(const Task *__restrict__ t
       double v = 0.0;
       if (col < cols && c < k) {
         if (MODE == 0)
-          v = hash_uniform((uint64_t)B.gid, (uint64_t)col, (uint64_t)c);
+          v = hash_uniform((uint64_t)B.gid, (uint32_t)col, (uint32_t)c);
         else
           v = X[(int64_t)c * cols + col];  // Q is |I| x k col-major (ld = m = cols)
       }
@@ -133,15 +141,15 @@ __global__ void __launch_bounds__(THREADS) k_gemm_gen(const Task *__restrict__ t
     __syncthreads();
 #pragma unroll
     for (int jj = 0; jj < GT_K; ++jj) {
-      double a[4], x[4];
+      double a[4], x[TC];
 #pragma unroll
       for (int q = 0; q < 4; ++q) a[q] = As[jj][ty * 4 + q];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) x[q] = Xs[jj][tx * 4 + q];
+      for (int q = 0; q < TC; ++q) x[q] = Xs[jj][tx * TC + q];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = __fma_rn(a[r], x[c], acc[r][c]);
+        for (int c = 0; c < TC; ++c) acc[r][c] = __fma_rn(a[r], x[c], acc[r][c]);
     }
   }
   double *Y = ws + (MODE == 0 ? B.oy : B.oz);
@@ -151,8 +159,8 @@ __global__ void __launch_bounds__(THREADS) k_gemm_gen(const Task *__restrict__ t
     int64_t row = T.r0 + ty * 4 + r;
     if (row >= rows) continue;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      int cc = c0 + tx * 4 + c;
+    for (int c = 0; c < TC; ++c) {
+      int cc = c0 + tx * TC + c;
       if (cc >= k) continue;
       Y[(int64_t)cc * rows + row] = acc[r][c];
       if (MODE == 1) Y2[(int64_t)cc * rows + row] = acc[r][c];
@@ -701,7 +709,8 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
     partb.alloc(sizeof(double) * 2 * std::max<size_t>(1, tR.size()));
     int kmax = 0;
     for (auto &c : blks) kmax = std::max(kmax, c.k);
-    const int gy = (kmax + GT_N - 1) / GT_N;
+    const bool narrow = kmax <= 32;  // 32-column tiles when every sketch of the batch fits
+    const int gy = narrow ? 1 : (kmax + 63) / 64;
     const Task *dA = taskb.as<Task>(), *dB = dA + tA.size(), *dR = dB + tB.size();
     double *ws = wsb.as<double>();
     CBlk *db = blkb.as<CBlk>();
@@ -709,7 +718,10 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
     // Y = A Omega
     for (size_t t0 = 0; t0 < tA.size(); t0 += 65535) {
       dim3 g((unsigned)std::min<size_t>(65535, tA.size() - t0), gy);
-      k_gemm_gen<0><<<g, THREADS, 0, st>>>(dA + t0, db, ws, pts, H->N, H->d, K);
+      if (narrow)
+        k_gemm_gen<0, 32><<<g, THREADS, 0, st>>>(dA + t0, db, ws, pts, H->N, H->d, K);
+      else
+        k_gemm_gen<0, 64><<<g, THREADS, 0, st>>>(dA + t0, db, ws, pts, H->N, H->d, K);
       HH_LAUNCHED();
     }
     mark(1);
@@ -719,7 +731,10 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
     // Z = A^T Q (and a copy for the R-only QR)
     for (size_t t0 = 0; t0 < tB.size(); t0 += 65535) {
       dim3 g((unsigned)std::min<size_t>(65535, tB.size() - t0), gy);
-      k_gemm_gen<1><<<g, THREADS, 0, st>>>(dB + t0, db, ws, pts, H->N, H->d, K);
+      if (narrow)
+        k_gemm_gen<1, 32><<<g, THREADS, 0, st>>>(dB + t0, db, ws, pts, H->N, H->d, K);
+      else
+        k_gemm_gen<1, 64><<<g, THREADS, 0, st>>>(dB + t0, db, ws, pts, H->N, H->d, K);
       HH_LAUNCHED();
     }
     mark(3);

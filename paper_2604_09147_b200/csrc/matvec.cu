@@ -27,25 +27,39 @@ namespace hh {
 
 namespace mv {
 
-constexpr int NCW = 8;                 // consumer warps
+#ifndef HH_MV_NCW
+#define HH_MV_NCW 8
+#endif
+constexpr int NCW = HH_MV_NCW;         // consumer warps
 constexpr int NCT = NCW * 32;          // consumer threads
 constexpr int THREADS = NCT + 32;      // + one producer warp
-constexpr int WDATA = 16384;           // factor bytes per stage
-constexpr int WBUF = WDATA + 32;       // + 16-B alignment slack on both ends
+#ifndef HH_MV_MINB
+#define HH_MV_MINB 1
+#endif
+// Stage geometry.  Measured on B200 (profiles/r01_variants.txt): fewer, larger stages with
+// more CTAs per SM win — 2 stages of 32 KiB factor data at 3 CTAs/SM for NR <= 2; the
+// FP64-bound multi-RHS kernels (NR >= 4) keep 3 stages at 1 CTA/SM.
+#ifndef HH_MV_WDATA
+#define HH_MV_WDATA 32768
+#endif
+#ifndef HH_MV_XDATA
+#define HH_MV_XDATA 4096
+#endif
+#ifndef HH_MV_STAGES
+#define HH_MV_STAGES 2
+#endif
 constexpr int META = 64;
 
 template <int NR> struct Geo {
-  static constexpr int XDATA = NR <= 2 ? 2048 : 8192;     // vector bytes per stage
-  static constexpr int XELEMS = XDATA / 8;                // doubles (rows x NR)
+  static constexpr int WDATA = HH_MV_WDATA;                       // factor bytes per stage
+  static constexpr int WBUF = WDATA + 32;                            // + 16-B alignment slack
+  static constexpr int XDATA = NR <= 2 ? HH_MV_XDATA : 8192;      // vector bytes per stage
+  static constexpr int XELEMS = XDATA / 8;                        // doubles (rows x NR)
   static constexpr int XBUF = XDATA + 32;
   static constexpr int STAGE = WBUF + XBUF + META;
-#ifdef HH_MV_STAGES
-  static constexpr int STAGES = HH_MV_STAGES;
-#else
-  static constexpr int STAGES = NR == 2 ? 5 : 6;
-#endif
+  static constexpr int STAGES = NR <= 2 ? HH_MV_STAGES : 3;
   static constexpr size_t smem(bool red) {
-    return (size_t)STAGES * STAGE + 2 * STAGES * sizeof(uint64_t) + (red ? sizeof(double) * NCT * NR : 0);
+    return (size_t)STAGES * STAGE + 2 * STAGES * sizeof(uint64_t) + (red ? sizeof(double) * NCT * NR * (NR >= 8 ? 2 : 1) : 0);
   }
 };
 
@@ -111,6 +125,10 @@ __device__ __forceinline__ int stage_copy(uint8_t *dst, const uint8_t *src, int6
   }
   return (int)(s - sa);
 }
+// arena base by tag without dynamic indexing of the kernel-parameter array (no local memory)
+__device__ __forceinline__ const uint8_t *pick(const uint8_t *const (&arr)[4], int t) {
+  return t == 0 ? arr[0] : t == 1 ? arr[1] : t == 2 ? arr[2] : arr[3];
+}
 __device__ __forceinline__ uint32_t window_bytes(const uint8_t *src, int64_t bytes) {
   const uintptr_t s = (uintptr_t)src;
   return bytes > 0 ? (uint32_t)(((s + bytes + 15) & ~(uintptr_t)15) - (s & ~(uintptr_t)15)) : 0u;
@@ -123,9 +141,6 @@ template <> struct Elem<TAG_FP16> { using T = __half; };
 template <> struct Elem<TAG_BF16> { using T = uint16_t; };
 
 // Tunables (compile-time; scripts/variants.sh builds alternatives side by side).
-#ifndef HH_MV_CHAINS
-#define HH_MV_CHAINS 4   // independent fp64 accumulation chains per thread at NR = 1
-#endif
 #ifndef HH_MV_CVT
 #define HH_MV_CVT 0      // 0: F2F conversion; 1: bit placement + exact power-of-two DMUL
 #endif
@@ -179,57 +194,45 @@ struct P1Args {
   int *ctr;
 };
 
-// Independent accumulation chains per thread: enough to cover the fp64 FMA latency with
-// the few warps per scheduler a 2-CTA/SM persistent kernel has.
-template <int NR> constexpr int chains() { return NR >= HH_MV_CHAINS ? 1 : HH_MV_CHAINS / NR; }
+// Register blocking: at NR >= 8 each thread owns MB = 2 factor columns (phase 1) or rows
+// (phase 2), so every vector entry loaded from shared memory feeds 2 * NR fp64 FMAs.
+template <int NR> constexpr int mblock() { return NR >= 8 ? 2 : 1; }
 
-// Generic strided dot-accumulate: acc[k] += sum_j up(e[j * es]) * v[j * vs + k] for the j
-// this thread owns (j = 0 .. cnt-1), with CH interleaved partial sums merged in fixed order.
-template <int TAG, int NR>
-__device__ __forceinline__ void strided_acc(const typename Elem<TAG>::T *e, const double *v, int cnt, int es,
-                                            int vs, double (&acc)[NR]) {
-  constexpr int CH = chains<NR>();
-  double part[CH][NR];
+// Strided dot-accumulate over the cnt indices j this thread owns:
+//   acc[b][k] += up(e[j * es + b * eo]) * v[j * vs + k]      (b < MB with valid[b])
+// One fixed summation order per (b, k) => bitwise reproducible.
+template <int TAG, int NR, int MB>
+__device__ __forceinline__ void block_acc(const typename Elem<TAG>::T *e, const double *v, int cnt, int es, int eo,
+                                          int vs, const bool (&valid)[MB], double (&acc)[MB][NR]) {
+#pragma unroll 2
+  for (int j = 0; j < cnt; ++j) {
+    double a[MB];
 #pragma unroll
-  for (int h = 0; h < CH; ++h)
+    for (int b = 0; b < MB; ++b) a[b] = valid[b] ? up<TAG>(e[b * eo]) : 0.0;
+    if constexpr (NR % 2 == 0) {  // 16-B aligned vector entries (NR * 8 bytes per index)
+      const double2 *v2 = reinterpret_cast<const double2 *>(v);
 #pragma unroll
-    for (int k = 0; k < NR; ++k) part[h][k] = 0.0;
-  int j = 0;
-  for (; j + CH <= cnt; j += CH) {
-    double a[CH];
+      for (int k2 = 0; k2 < NR / 2; ++k2) {
+        const double2 xv = v2[k2];
 #pragma unroll
-    for (int h = 0; h < CH; ++h) a[h] = up<TAG>(e[h * es]);
+        for (int b = 0; b < MB; ++b) {
+          acc[b][2 * k2] = __fma_rn(a[b], xv.x, acc[b][2 * k2]);
+          acc[b][2 * k2 + 1] = __fma_rn(a[b], xv.y, acc[b][2 * k2 + 1]);
+        }
+      }
+    } else {
 #pragma unroll
-    for (int h = 0; h < CH; ++h)
+      for (int k = 0; k < NR; ++k)
 #pragma unroll
-      for (int k = 0; k < NR; ++k) part[h][k] = __fma_rn(a[h], v[h * vs + k], part[h][k]);
-    e += CH * es;
-    v += CH * vs;
-  }
-  for (; j < cnt; ++j) {
-    const double a0 = up<TAG>(e[0]);
-#pragma unroll
-    for (int k = 0; k < NR; ++k) part[0][k] = __fma_rn(a0, v[k], part[0][k]);
+        for (int b = 0; b < MB; ++b) acc[b][k] = __fma_rn(a[b], v[k], acc[b][k]);
+    }
     e += es;
     v += vs;
   }
-#pragma unroll
-  for (int h = 0; h < CH; ++h)
-#pragma unroll
-    for (int k = 0; k < NR; ++k) acc[k] += part[h][k];
-}
-
-// rows [0, nrows) of the staged window; thread (c, q) takes rows q, q + Q, ...
-template <int TAG, int NR>
-__device__ __forceinline__ void p1_rows(const uint8_t *wst, const double *xst, int nrows, int ct, int c, int q,
-                                        int Q, double (&acc)[NR]) {
-  using T = typename Elem<TAG>::T;
-  const int cnt = q < nrows ? (nrows - q + Q - 1) / Q : 0;
-  strided_acc<TAG, NR>(reinterpret_cast<const T *>(wst) + q * ct + c, xst + q * NR, cnt, Q * ct, Q * NR, acc);
 }
 
 template <int NR>
-__global__ void __launch_bounds__(THREADS) k_phase1(P1Args a) {
+__global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
   using G = Geo<NR>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
@@ -253,8 +256,8 @@ __global__ void __launch_bounds__(THREADS) k_phase1(P1Args a) {
       const int nxt = atomicAdd(a.ctr, 1);
       const int w = tag_bytes(T.tag);
       const int rowb = T.ct * w;
-      const int rs = max(1, min(G::XELEMS / NR, WDATA / rowb));
-      const uint8_t *wbase = a.W[T.tag] + T.src;
+      const int rs = max(1, min(G::XELEMS / NR, G::WDATA / rowb));
+      const uint8_t *wbase = pick(a.W, T.tag) + T.src;
       const uint8_t *xbase = reinterpret_cast<const uint8_t *>(a.v + T.x0 * NR);
       for (int r0 = 0; r0 < T.n; r0 += rs, ++n) {
         const int r1 = min(T.n, r0 + rs);
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(THREADS) k_phase1(P1Args a) {
         const int64_t wlen = (int64_t)(r1 - r0) * rowb;
         const uint8_t *xsrc = xbase + (int64_t)r0 * NR * 8;
         const int64_t xlen = (int64_t)(r1 - r0) * NR * 8;
-        Meta *m = reinterpret_cast<Meta *>(st + WBUF + G::XBUF);
+        Meta *m = reinterpret_cast<Meta *>(st + G::WBUF + G::XBUF);
         m->kind = 0;
         m->wlead = (int)((uintptr_t)wsrc & 15);
         m->xlead = (int)((uintptr_t)xsrc & 15);
@@ -278,44 +281,67 @@ __global__ void __launch_bounds__(THREADS) k_phase1(P1Args a) {
         mbar_expect_tx(&full[s], window_bytes(wsrc, wlen) + window_bytes(xsrc, xlen));
         uint32_t tx = 0;
         stage_copy(st, wsrc, wlen, &full[s], pol_w, tx);
-        stage_copy(st + WBUF, xsrc, xlen, &full[s], pol_x, tx);
+        stage_copy(st + G::WBUF, xsrc, xlen, &full[s], pol_x, tx);
       }
       item = nxt;
     }
     const int s = n % G::STAGES;
     if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
-    reinterpret_cast<Meta *>(smem + s * G::STAGE + WBUF + G::XBUF)->kind = 1;
+    reinterpret_cast<Meta *>(smem + s * G::STAGE + G::WBUF + G::XBUF)->kind = 1;
     mbar_arrive(&full[s]);
     return;
   }
   // --------------------------------------------------------------------- consumers
+  constexpr int MB = mblock<NR>();
   const int tid = threadIdx.x;
-  double acc[NR];
-  int32_t zi = 0;
+  double acc[MB][NR];
+  int32_t zi[MB];
   for (int n = 0;; ++n) {
     const int s = n % G::STAGES;
     mbar_wait(&full[s], (n / G::STAGES) & 1);
     const uint8_t *st = smem + s * G::STAGE;
-    const Meta m = *reinterpret_cast<const Meta *>(st + WBUF + G::XBUF);
+    const Meta m = *reinterpret_cast<const Meta *>(st + G::WBUF + G::XBUF);
     if (m.kind) break;
     const int ct = m.a;
-    const int Q = ct > 128 ? 1 : ct > 64 ? 2 : ct > 32 ? 4 : 8;   // row groups (power of two)
-    const int c = tid / Q, q = tid % Q;
-    const bool active = c < ct;
+    const int slots = (ct + MB - 1) / MB;  // thread column slot cs owns columns cs + b * slots
+    int Q = 1;  // row groups: power of two <= 8 with Q * slots <= NCT (a column's lanes share a warp)
+    while (Q < 8 && 2 * Q * slots <= NCT) Q <<= 1;
+    const int cs = tid / Q, q = tid % Q;
+    const bool active = cs < slots;
+    bool valid[MB];
+#pragma unroll
+    for (int b = 0; b < MB; ++b) valid[b] = active && cs + b * slots < ct;
     if (m.r0 == 0) {
 #pragma unroll
-      for (int k = 0; k < NR; ++k) acc[k] = 0.0;
-      if (active && q == 0) zi = a.zmap[m.p + c];
+      for (int b = 0; b < MB; ++b) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) acc[b][k] = 0.0;
+        if (valid[b] && q == 0) zi[b] = a.zmap[m.p + cs + b * slots];
+      }
     }
     if (active) {
       const uint8_t *wst = st + m.wlead;
-      const double *xst = reinterpret_cast<const double *>(st + WBUF + m.xlead);
+      const double *xst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
       const int nrows = m.r1 - m.r0;
+      const int cnt = q < nrows ? (nrows - q + Q - 1) / Q : 0;
+      const int e0 = q * ct + cs;
       switch (m.b) {
-        case TAG_FP64: p1_rows<TAG_FP64, NR>(wst, xst, nrows, ct, c, q, Q, acc); break;
-        case TAG_FP32: p1_rows<TAG_FP32, NR>(wst, xst, nrows, ct, c, q, Q, acc); break;
-        case TAG_FP16: p1_rows<TAG_FP16, NR>(wst, xst, nrows, ct, c, q, Q, acc); break;
-        default: p1_rows<TAG_BF16, NR>(wst, xst, nrows, ct, c, q, Q, acc); break;
+        case TAG_FP64:
+          block_acc<TAG_FP64, NR, MB>(reinterpret_cast<const double *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
+                                      Q * NR, valid, acc);
+          break;
+        case TAG_FP32:
+          block_acc<TAG_FP32, NR, MB>(reinterpret_cast<const float *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
+                                      Q * NR, valid, acc);
+          break;
+        case TAG_FP16:
+          block_acc<TAG_FP16, NR, MB>(reinterpret_cast<const __half *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
+                                      Q * NR, valid, acc);
+          break;
+        default:
+          block_acc<TAG_BF16, NR, MB>(reinterpret_cast<const uint16_t *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
+                                      Q * NR, valid, acc);
+          break;
       }
     }
     __syncwarp();
@@ -323,12 +349,17 @@ __global__ void __launch_bounds__(THREADS) k_phase1(P1Args a) {
     if (m.r1 == m.q) {  // last stage of the tile: fixed-order reduction over the Q row groups
       for (int o = 1; o < Q; o <<= 1)
 #pragma unroll
-        for (int k = 0; k < NR; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-      if (active && q == 0) {
-        double *out = a.v + (a.N + zi) * NR;
+        for (int b = 0; b < MB; ++b)
 #pragma unroll
-        for (int k = 0; k < NR; ++k) out[k] = acc[k];
-      }
+          for (int k = 0; k < NR; ++k) acc[b][k] += __shfl_xor_sync(0xffffffffu, acc[b][k], o);
+      if (q == 0)
+#pragma unroll
+        for (int b = 0; b < MB; ++b)
+          if (valid[b]) {
+            double *out = a.v + (a.N + zi[b]) * NR;
+#pragma unroll
+            for (int k = 0; k < NR; ++k) out[k] = acc[b][k];
+          }
     }
   }
 }
@@ -347,22 +378,13 @@ struct P2Args {
   int *ctr;
 };
 
-// columns [0, ncols) of the staged window; thread (row rr, group g) takes g, g + G, ...
-template <int TAG, int NR>
-__device__ __forceinline__ void p2_cols(const uint8_t *ust, const double *zst, int ncols, int nr, int rr, int g, int G,
-                                        double (&acc)[NR]) {
-  using T = typename Elem<TAG>::T;
-  const int cnt = g < ncols ? (ncols - g + G - 1) / G : 0;
-  strided_acc<TAG, NR>(reinterpret_cast<const T *>(ust) + g * nr + rr, zst + g * NR, cnt, G * nr, G * NR, acc);
-}
-
 template <int NR>
-__global__ void __launch_bounds__(THREADS) k_phase2(P2Args a) {
+__global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
   using G = Geo<NR>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
   uint64_t *empty = full + G::STAGES;
-  double *red = reinterpret_cast<double *>(empty + G::STAGES);  // [NCT][NR]
+  double *red = reinterpret_cast<double *>(empty + G::STAGES);  // [NCT][MB][NR]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < G::STAGES; ++s) {
@@ -384,8 +406,8 @@ __global__ void __launch_bounds__(THREADS) k_phase2(P2Args a) {
         const P2Seg S = a.segs[si];
         const int w = tag_bytes(S.tag);
         const int colb = Lf.nr * w;
-        const int cs = max(1, min(G::XELEMS / NR, WDATA / colb));
-        const uint8_t *ubase = (S.dense ? a.D : a.U[S.tag]) + S.src;
+        const int cs = max(1, min(G::XELEMS / NR, G::WDATA / colb));
+        const uint8_t *ubase = (S.dense ? a.D : pick(a.U, S.tag)) + S.src;
         const uint8_t *zbase = reinterpret_cast<const uint8_t *>(a.v + S.vbeg * NR);
         for (int c0 = 0; c0 < S.ncols; c0 += cs, ++n) {
           const int c1 = min(S.ncols, c0 + cs);
@@ -396,7 +418,7 @@ __global__ void __launch_bounds__(THREADS) k_phase2(P2Args a) {
           const int64_t ulen = (int64_t)(c1 - c0) * colb;
           const uint8_t *zsrc = zbase + (int64_t)c0 * NR * 8;
           const int64_t zlen = (int64_t)(c1 - c0) * NR * 8;
-          Meta *m = reinterpret_cast<Meta *>(st + WBUF + G::XBUF);
+          Meta *m = reinterpret_cast<Meta *>(st + G::WBUF + G::XBUF);
           m->kind = 0;
           m->wlead = (int)((uintptr_t)usrc & 15);
           m->xlead = (int)((uintptr_t)zsrc & 15);
@@ -409,62 +431,93 @@ __global__ void __launch_bounds__(THREADS) k_phase2(P2Args a) {
           mbar_expect_tx(&full[s], window_bytes(usrc, ulen) + window_bytes(zsrc, zlen));
           uint32_t tx = 0;
           stage_copy(st, usrc, ulen, &full[s], pol_w, tx);
-          stage_copy(st + WBUF, zsrc, zlen, &full[s], pol_x, tx);
+          stage_copy(st + G::WBUF, zsrc, zlen, &full[s], pol_x, tx);
         }
       }
       li = nxt;
     }
     const int s = n % G::STAGES;
     if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
-    reinterpret_cast<Meta *>(smem + s * G::STAGE + WBUF + G::XBUF)->kind = 1;
+    reinterpret_cast<Meta *>(smem + s * G::STAGE + G::WBUF + G::XBUF)->kind = 1;
     mbar_arrive(&full[s]);
     return;
   }
   // --------------------------------------------------------------------- consumers
+  constexpr int MB = mblock<NR>();
   const int tid = threadIdx.x;
-  double acc[NR];
+  double acc[MB][NR];
 #pragma unroll
-  for (int k = 0; k < NR; ++k) acc[k] = 0.0;
+  for (int b = 0; b < MB; ++b)
+#pragma unroll
+    for (int k = 0; k < NR; ++k) acc[b][k] = 0.0;
   for (int n = 0;; ++n) {
     const int s = n % G::STAGES;
     mbar_wait(&full[s], (n / G::STAGES) & 1);
     const uint8_t *st = smem + s * G::STAGE;
-    const Meta m = *reinterpret_cast<const Meta *>(st + WBUF + G::XBUF);
+    const Meta m = *reinterpret_cast<const Meta *>(st + G::WBUF + G::XBUF);
     if (m.kind) break;
     const int nr = m.a;
-    const int Gn = NCT / nr;  // nr <= 256 (leaf_size limit)
-    const int rr = tid % nr, g = tid / nr;
+    const int nr2 = (nr + MB - 1) / MB;  // thread row slot rr owns rows rr + b * nr2
+    const int Gn = NCT / nr2;            // column groups (nr <= 256: leaf_size limit)
+    const int rr = tid % nr2, g = tid / nr2;
+    bool valid[MB];
+#pragma unroll
+    for (int b = 0; b < MB; ++b) valid[b] = g < Gn && rr + b * nr2 < nr;
     if (g < Gn) {
       const uint8_t *ust = st + m.wlead;
-      const double *zst = reinterpret_cast<const double *>(st + WBUF + m.xlead);
+      const double *zst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
       const int ncols = m.r1 - m.r0;
+      const int cnt = g < ncols ? (ncols - g + Gn - 1) / Gn : 0;
+      const int e0 = g * nr + rr;
       switch (m.b & 0xff) {
-        case TAG_FP64: p2_cols<TAG_FP64, NR>(ust, zst, ncols, nr, rr, g, Gn, acc); break;
-        case TAG_FP32: p2_cols<TAG_FP32, NR>(ust, zst, ncols, nr, rr, g, Gn, acc); break;
-        case TAG_FP16: p2_cols<TAG_FP16, NR>(ust, zst, ncols, nr, rr, g, Gn, acc); break;
-        default: p2_cols<TAG_BF16, NR>(ust, zst, ncols, nr, rr, g, Gn, acc); break;
+        case TAG_FP64:
+          block_acc<TAG_FP64, NR, MB>(reinterpret_cast<const double *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
+                                      Gn * NR, valid, acc);
+          break;
+        case TAG_FP32:
+          block_acc<TAG_FP32, NR, MB>(reinterpret_cast<const float *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
+                                      Gn * NR, valid, acc);
+          break;
+        case TAG_FP16:
+          block_acc<TAG_FP16, NR, MB>(reinterpret_cast<const __half *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
+                                      Gn * NR, valid, acc);
+          break;
+        default:
+          block_acc<TAG_BF16, NR, MB>(reinterpret_cast<const uint16_t *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
+                                      Gn * NR, valid, acc);
+          break;
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (m.flags & 1) {  // last stage of the leaf: fixed-order reduction over groups, scatter (a10)
 #pragma unroll
-      for (int k = 0; k < NR; ++k) red[tid * NR + k] = acc[k];
+      for (int b = 0; b < MB; ++b)
+#pragma unroll
+        for (int k = 0; k < NR; ++k) red[(tid * MB + b) * NR + k] = acc[b][k];
       consumer_sync();
-      if (tid < nr) {
-        double sum[NR];
+      if (tid < nr2) {
 #pragma unroll
-        for (int k = 0; k < NR; ++k) sum[k] = 0.0;
-        for (int gg = 0; gg < Gn; ++gg)
+        for (int b = 0; b < MB; ++b) {
+          const int r = tid + b * nr2;
+          if (r < nr) {
+            double sum[NR];
 #pragma unroll
-          for (int k = 0; k < NR; ++k) sum[k] += red[(gg * nr + tid) * NR + k];
-        const int64_t i = a.perm[m.p + tid];
+            for (int k = 0; k < NR; ++k) sum[k] = 0.0;
+            for (int gg = 0; gg < Gn; ++gg)
 #pragma unroll
-        for (int k = 0; k < NR; ++k) a.y[i + k * a.ldy] = sum[k];
+              for (int k = 0; k < NR; ++k) sum[k] += red[((gg * nr2 + tid) * MB + b) * NR + k];
+            const int64_t i = a.perm[m.p + r];
+#pragma unroll
+            for (int k = 0; k < NR; ++k) a.y[i + k * a.ldy] = sum[k];
+          }
+        }
       }
       consumer_sync();
 #pragma unroll
-      for (int k = 0; k < NR; ++k) acc[k] = 0.0;
+      for (int b = 0; b < MB; ++b)
+#pragma unroll
+        for (int k = 0; k < NR; ++k) acc[b][k] = 0.0;
     }
   }
 }
