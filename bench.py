@@ -90,6 +90,30 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ----------------------------------------------------------------------------- context
+PAPER_CONTEXT = ("paper (context, not the target): adaptive mixed-precision H_h stores up to ~11x less than "
+                 "uniform-fp64 standard H (3D Matern/Gauss, eps=1e-2, N=125000) and ~4.8x (2D log, eps=1e-2); "
+                 "ratio 1 for eps<=1e-10; all errors within Thm 4.2/4.4 bounds; serial MATLAB R2024a on a Xeon "
+                 "Gold 2.6 GHz with chop-simulated precisions, no runtime reported (PAPER.md:6, 1121-1123, "
+                 "1202-1203, 1264)")
+
+
+def storage_ratio(config: str, stored: int):
+    """Stored bytes of uniform-fp64 standard-admissibility H (switch NONE) over ours, from the
+    ledger-only build recorded by scripts/sweep.py (profiles/r01_sweep.jsonl), if present."""
+    path = os.path.join(ROOT, "profiles", "r01_sweep.jsonl")
+    try:
+        for line in open(path):
+            r = json.loads(line)
+            if r.get("config") == config and r.get("switch_level") == "none" and r.get("precision") == "fp64":
+                return {"vs_uniform_fp64_standard_H": round(r["stored_bytes"] / stored, 3),
+                        "fp64_standard_H_bytes": r["stored_bytes"], "source": "profiles/r01_sweep.jsonl"
+                        + (" (ledger-only build)" if r.get("ledger_only") else "")}
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
+
+
 # ----------------------------------------------------------------------------- multi-rank plumbing
 def max_over_ranks(x: float, device=None) -> float:
     """Max over ranks of a per-rank device time (replicas: the job ends with the slowest
@@ -318,6 +342,8 @@ def run_ours(args, rank, world, local_rank):
                      "phase1_GBps": round(w_bytes / (p1_ms / 1e3) / 1e9, 1) if p1_ms else None,
                      "phase2_GBps": round((u_bytes + d_bytes) / (p2_ms / 1e3) / 1e9, 1) if p2_ms else None},
         "e2e": e2e,
+        "storage_ratio": storage_ratio("sweep" if args.config == "sweep" else args.config, stored),
+        "paper_context": PAPER_CONTEXT,
         "gpu_launches": int(launches),
         "clocks": clocks,
     }

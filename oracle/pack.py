@@ -10,7 +10,7 @@ Layout (byte offsets; ALIGN = 16):
   W[g]  : source panels.  Tag-g low-rank blocks with p > 0 ordered by (level, src, tgt); a
           run of equal (level, src) is one panel: an n x P matrix (n = |src cluster|, P = sum
           of the run's ranks) whose columns are the blocks' W_b columns in that order
-          (wcol[b] = first column of b).  The panel is cut into column tiles of CT = 256
+          (wcol[b] = first column of b).  The panel is cut into column tiles of CT = 248
           columns (the last one narrower); each tile is stored row-major (element (r, j) of a
           tile of width ct at r * ct + j) and starts at a multiple of ALIGN; tiles follow each
           other in column order.  w_off[b] = byte offset of the panel's first tile.
@@ -29,7 +29,7 @@ import numpy as np
 from . import formats as F
 
 ALIGN = 16
-CT = 256          # W panel column-tile width
+CT = 248          # W panel column-tile width (W_CT in csrc/handle.h)
 LR, DENSE = 0, 1
 
 

@@ -39,7 +39,7 @@ template <class T> void h2d(DBuf &b, const std::vector<T> &v, cudaStream_t s) {
 // W panels: for each (tag, level, source cluster J) the tag's low-rank blocks
 // with source J, in target order, form one |J| x P_J panel (P_J = sum of their ranks) split
 // into column tiles of width <= W_CT, each stored row-major and 16-B aligned.
-constexpr int W_CT = 256;
+constexpr int W_CT = 248;  // row stride = 24 (fp32) / 28 (16-bit) banks mod 32: conflict-free 4-row DMMA fragments
 
 // Phase-1 work item: one column tile of one W panel (all |J| rows).
 struct P1Tile {

@@ -4,7 +4,7 @@
 //                 counters of the two persistent kernels
 //   a8  phase 1:  z_b = W_b^T x_J for every low-rank block.  W is stored as per-source
 //                 panels: for a source cluster J all blocks b with src J form
-//                 one |J| x P_J matrix, cut into column tiles of <= 256 columns stored
+//                 one |J| x P_J matrix, cut into column tiles of <= 248 columns stored
 //                 row-major.  One work item = one tile; thread c of the CTA owns tile column
 //                 c and accumulates it over all |J| rows, so z needs no second pass.
 //   a9  phase 2:  per leaf R (one owner, fixed order, no atomics):
@@ -50,16 +50,26 @@ constexpr int THREADS = NCT + 32;      // + one producer warp
 #endif
 constexpr int META = 64;
 
+// FP64 tensor-core (DMMA m8n8k4) consumers for the multi-RHS contractions (NR = 8, 16):
+// the phase-1 tile is then D = W^T X (ct x NR) and the phase-2 leaf Y = U Z (nr x NR).
+#ifndef HH_MV_MMA
+#define HH_MV_MMA 1
+#endif
+template <int NR> constexpr bool use_mma() { return HH_MV_MMA && (NR == 8 || NR == 16); }
+
 template <int NR> struct Geo {
   static constexpr int WDATA = HH_MV_WDATA;                       // factor bytes per stage
   static constexpr int WBUF = WDATA + 32;                            // + 16-B alignment slack
-  static constexpr int XDATA = NR <= 2 ? HH_MV_XDATA : 8192;      // vector bytes per stage
+  static constexpr int XDATA = NR <= 2 ? HH_MV_XDATA : NR * 2048;  // vector bytes per stage
   static constexpr int XELEMS = XDATA / 8;                        // doubles (rows x NR)
   static constexpr int XBUF = XDATA + 32;
   static constexpr int STAGE = WBUF + XBUF + META;
-  static constexpr int STAGES = NR <= 2 ? HH_MV_STAGES : 3;
+  static constexpr int STAGES = HH_MV_STAGES;
+  static constexpr size_t red_bytes() {  // phase-2 cross-group reduction buffer
+    return use_mma<NR>() ? sizeof(double) * NCW * 4 * (NR / 8) * 32 * 2 : sizeof(double) * NCT * NR * (NR >= 8 ? 2 : 1);
+  }
   static constexpr size_t smem(bool red) {
-    return (size_t)STAGES * STAGE + 2 * STAGES * sizeof(uint64_t) + (red ? sizeof(double) * NCT * NR * (NR >= 8 ? 2 : 1) : 0);
+    return (size_t)STAGES * STAGE + 2 * STAGES * sizeof(uint64_t) + (red ? red_bytes() : 0);
   }
 };
 
@@ -171,6 +181,14 @@ __device__ __forceinline__ double up(const typename Elem<TAG>::T v) {
   }
 }
 
+// D = A B + D on the FP64 tensor cores: A 8x4 (thread holds A[lane/4][lane%4]), B 4x8
+// (thread holds B[lane%4][lane/4]), C/D 8x8 (thread holds row lane/4, columns 2(lane%4)+{0,1}).
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
 // --------------------------------------------------------------------------- gather
 template <int NR>
 __global__ void k_gather(const int32_t *__restrict__ perm, const double *__restrict__ x, int64_t N, int64_t ldx,
@@ -228,6 +246,85 @@ __device__ __forceinline__ void block_acc(const typename Elem<TAG>::T *e, const 
     }
     e += es;
     v += vs;
+  }
+}
+
+// Phase-1 DMMA consumer (NR = 8, 16): warp w owns tile columns [32w, 32w + 32) as four
+// 8-column M-tiles; each 4-row K-step does 4 x NR/8 DMMAs.  Accumulators persist over the
+// tile's row windows; z is written at the last one.
+template <int TAG, int NR>
+__device__ __forceinline__ void p1_mma_rows(const uint8_t *wst, const double *xst, int nrows, int ct, int col0,
+                                            int lane, double (&c)[4][NR / 8][2]) {
+  using T = typename Elem<TAG>::T;
+  const T *W = reinterpret_cast<const T *>(wst);
+  const int kq = lane & 3, mq = lane >> 2;
+  bool cv[4];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) cv[mt] = col0 + mt * 8 + mq < ct;
+#pragma unroll 2
+  for (int k0 = 0; k0 < nrows; k0 += 4) {
+    const int row = k0 + kq;
+    const bool rv = row < nrows;
+    double b[NR / 8];
+#pragma unroll
+    for (int nt = 0; nt < NR / 8; ++nt) b[nt] = rv ? xst[row * NR + nt * 8 + mq] : 0.0;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const double av = (rv && cv[mt]) ? up<TAG>(W[row * ct + col0 + mt * 8 + mq]) : 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NR / 8; ++nt) dmma(c[mt][nt], av, b[nt]);
+    }
+  }
+}
+
+template <int NR, class G>
+__device__ __forceinline__ void p1_mma_consumer(const P1Args &a, uint8_t *smem, uint64_t *full, uint64_t *empty,
+                                                int warp, int lane) {
+  constexpr int NT = NR / 8;
+  double c[4][NT][2];
+  int32_t zi[4];
+  for (int n = 0;; ++n) {
+    const int s = n % G::STAGES;
+    mbar_wait(&full[s], (n / G::STAGES) & 1);
+    const uint8_t *st = smem + s * G::STAGE;
+    const Meta m = *reinterpret_cast<const Meta *>(st + G::WBUF + G::XBUF);
+    if (m.kind) break;
+    const int ct = m.a, col0 = warp * 32;
+    const bool active = col0 < ct;
+    if (m.r0 == 0) {
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
+        const int col = col0 + mt * 8 + (lane >> 2);
+        if (col < ct) zi[mt] = a.zmap[m.p + col];
+      }
+    }
+    if (active) {
+      const uint8_t *wst = st + m.wlead;
+      const double *xst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
+      const int nrows = m.r1 - m.r0;
+      switch (m.b) {
+        case TAG_FP64: p1_mma_rows<TAG_FP64, NR>(wst, xst, nrows, ct, col0, lane, c); break;
+        case TAG_FP32: p1_mma_rows<TAG_FP32, NR>(wst, xst, nrows, ct, col0, lane, c); break;
+        case TAG_FP16: p1_mma_rows<TAG_FP16, NR>(wst, xst, nrows, ct, col0, lane, c); break;
+        default: p1_mma_rows<TAG_BF16, NR>(wst, xst, nrows, ct, col0, lane, c); break;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (m.r1 == m.q && active) {
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int col = col0 + mt * 8 + (lane >> 2);
+        if (col < ct) {
+          double *out = a.v + (a.N + zi[mt]) * NR + 2 * (lane & 3);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            *reinterpret_cast<double2 *>(out + nt * 8) = make_double2(c[mt][nt][0], c[mt][nt][1]);
+        }
+      }
+    }
   }
 }
 
@@ -289,6 +386,10 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
     if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
     reinterpret_cast<Meta *>(smem + s * G::STAGE + G::WBUF + G::XBUF)->kind = 1;
     mbar_arrive(&full[s]);
+    return;
+  }
+  if constexpr (use_mma<NR>()) {
+    p1_mma_consumer<NR, G>(a, smem, full, empty, warp, lane);
     return;
   }
   // --------------------------------------------------------------------- consumers
@@ -378,6 +479,105 @@ struct P2Args {
   int *ctr;
 };
 
+// Phase-2 DMMA consumer (NR = 8, 16): the leaf's rows form ceil(nr/8) M-tiles, grouped by
+// four (MG groups); warp w takes group w % MG and the K-steps (4 columns) k = w / MG (mod
+// KS), KS = NCW / MG.  At the leaf's last window the KS partial tiles of each group are
+// summed in a fixed order through shared memory and scattered to y (a10).
+template <int TAG, int NR>
+__device__ __forceinline__ void p2_mma_cols(const uint8_t *ust, const double *zst, int ncols, int nr, int row0,
+                                            int kfirst, int KS, int lane, double (&c)[4][NR / 8][2]) {
+  using T = typename Elem<TAG>::T;
+  const T *U = reinterpret_cast<const T *>(ust);
+  const int kq = lane & 3, mq = lane >> 2;
+  bool rv[4];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) rv[mt] = row0 + mt * 8 + mq < nr;
+#pragma unroll 2
+  for (int k0 = 4 * kfirst; k0 < ncols; k0 += 4 * KS) {
+    const int col = k0 + kq;
+    const bool cvl = col < ncols;
+    double b[NR / 8];
+#pragma unroll
+    for (int nt = 0; nt < NR / 8; ++nt) b[nt] = cvl ? zst[col * NR + nt * 8 + mq] : 0.0;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const double av = (cvl && rv[mt]) ? up<TAG>(U[col * nr + row0 + mt * 8 + mq]) : 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NR / 8; ++nt) dmma(c[mt][nt], av, b[nt]);
+    }
+  }
+}
+
+template <int NR, class G>
+__device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, uint64_t *full, uint64_t *empty,
+                                                double *red, int warp, int lane) {
+  constexpr int NT = NR / 8;
+  double c[4][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
+  int kbase = 0;  // K-step parity offset: windows of a leaf continue the K-step numbering
+  for (int n = 0;; ++n) {
+    const int s = n % G::STAGES;
+    mbar_wait(&full[s], (n / G::STAGES) & 1);
+    const uint8_t *st = smem + s * G::STAGE;
+    const Meta m = *reinterpret_cast<const Meta *>(st + G::WBUF + G::XBUF);
+    if (m.kind) break;
+    const int nr = m.a;
+    const int MG = (nr + 31) / 32;
+    const int KS = max(1, NCW / MG);
+    const int mg = warp % MG, ks = warp / MG;
+    const bool active = warp < MG * KS;
+    const int ncols = m.r1 - m.r0;
+    if (active) {
+      const uint8_t *ust = st + m.wlead;
+      const double *zst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
+      const int kfirst = ((ks - kbase) % KS + KS) % KS;
+      switch (m.b & 0xff) {
+        case TAG_FP64: p2_mma_cols<TAG_FP64, NR>(ust, zst, ncols, nr, mg * 32, kfirst, KS, lane, c); break;
+        case TAG_FP32: p2_mma_cols<TAG_FP32, NR>(ust, zst, ncols, nr, mg * 32, kfirst, KS, lane, c); break;
+        case TAG_FP16: p2_mma_cols<TAG_FP16, NR>(ust, zst, ncols, nr, mg * 32, kfirst, KS, lane, c); break;
+        default: p2_mma_cols<TAG_BF16, NR>(ust, zst, ncols, nr, mg * 32, kfirst, KS, lane, c); break;
+      }
+    }
+    kbase = (kbase + (ncols + 3) / 4) % KS;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (m.flags & 1) {
+      double *mine = red + (size_t)warp * 4 * NT * 64;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          mine[((mt * NT + nt) * 32 + lane) * 2] = c[mt][nt][0];
+          mine[((mt * NT + nt) * 32 + lane) * 2 + 1] = c[mt][nt][1];
+          c[mt][nt][0] = c[mt][nt][1] = 0.0;
+        }
+      consumer_sync();
+      if (warp < MG) {  // ks == 0 warp of group mg: fixed-order sum over k-slices
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          const int r = mg * 32 + mt * 8 + (lane >> 2);
+          if (r >= nr) continue;
+          const int64_t i = a.perm[m.p + r];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              double sum = 0.0;
+              for (int k = 0; k < KS; ++k)
+                sum += red[(size_t)(mg + k * MG) * 4 * NT * 64 + ((mt * NT + nt) * 32 + lane) * 2 + h];
+              a.y[i + (int64_t)(nt * 8 + 2 * (lane & 3) + h) * a.ldy] = sum;
+            }
+        }
+      }
+      consumer_sync();
+      kbase = 0;
+    }
+  }
+}
+
 template <int NR>
 __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
   using G = Geo<NR>;
@@ -440,6 +640,10 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
     if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
     reinterpret_cast<Meta *>(smem + s * G::STAGE + G::WBUF + G::XBUF)->kind = 1;
     mbar_arrive(&full[s]);
+    return;
+  }
+  if constexpr (use_mma<NR>()) {
+    p2_mma_consumer<NR, G>(a, smem, full, empty, red, warp, lane);
     return;
   }
   // --------------------------------------------------------------------- consumers

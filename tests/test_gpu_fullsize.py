@@ -166,3 +166,35 @@ def test_full_check3_sampled_rows(full):
     r2 = float(np.sum((Ax[:, 0] - y[rows, 0]) ** 2))
     e_est = np.sqrt(r2 * N / rows.size) / (np.sqrt(fro2_rows * N / rows.size) * np.linalg.norm(x))
     assert e_est <= 10 * cfg["eps"], e_est
+
+
+def test_full_check4_mixed_vs_uniform_fp64(full):
+    """Check (4): mixed-precision error vs uniform-fp64 H_h on the same partition, within the
+    Thm 4.4 bound (measured sparsity constants) and the block-count form of the mixed-
+    precision increment; 3D N=2^20: uniform fp64 does not fit in HBM
+    (SURVEY.md §8(c)), so only the mixed bound is checked there."""
+    from oracle import metrics as M
+    name, cfg, P, H, ex, tr, part, lay = full
+    info = ex["info"]
+    x = W.make_rhs(cfg, 1)
+    rng = np.random.default_rng(11)
+    rows = rng.choice(cfg["N"], size=64, replace=False)
+    Ax, fro2_rows = D.dense_apply(P, cfg["kernel"], cfg["scale"], x, rows=rows, chunk=8)
+
+    def e_est(y):
+        return float(np.sqrt(np.sum((Ax[:, 0] - y[rows, 0]) ** 2) / fro2_rows) / np.linalg.norm(x))
+
+    e_amp = e_est(PL.gpu_matvec(H, x))
+    bound = M.thm44_factor(info["L"], cfg["s"], info["c_far"], info["c_nbr"], info["c_sib"]) * cfg["eps"]
+    assert e_amp <= bound
+    if name == "3d_large":
+        return
+    H64 = PL.gpu_build(P, cfg, pset=W.P_FP64)
+    try:
+        e64 = e_est(PL.gpu_matvec(H64, x))
+    finally:
+        hh.hh_free(H64)
+    B = ex["blocks"]
+    lv = B["level"][(B["storage"] == 0) & (B["rank"] > 0)].astype(float)
+    assert e64 <= bound
+    assert e_amp - e64 <= 2 * cfg["eps"] * np.sqrt(np.sum(2.0 ** (-cfg["d"] * lv))) + 1e-15
