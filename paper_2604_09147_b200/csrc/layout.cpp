@@ -244,8 +244,8 @@ void compute_layout(hh_matrix *H) {
 // ----------------------------------------------------------------- matvec work plan
 // Phase 1: one item per W column tile, largest first (the kernels take items from a work
 // counter, so big tiles start early).  zmap[zbase + c] = z index of tile column c.
-// Phase 2: per leaf, dense segments then per tag the levels' U column groups; leaves with
-// the most bytes first.
+// Phase 2: per leaf, dense segments then per tag the levels' U column groups; leaves in
+// Morton order.
 void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &zmap, std::vector<P2Seg> &segs,
                 std::vector<P2Leaf> &leaves) {
   const size_t nb = H->level.size();
@@ -342,14 +342,10 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
     leaves.push_back(lf);
     lbytes.push_back(bytes);
   }
-  {
-    std::vector<size_t> ord(leaves.size());
-    for (size_t k = 0; k < ord.size(); ++k) ord[k] = k;
-    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t c) { return lbytes[a] > lbytes[c]; });
-    std::vector<P2Leaf> l2(leaves.size());
-    for (size_t k = 0; k < ord.size(); ++k) l2[k] = leaves[ord[k]];
-    leaves.swap(l2);
-  }
+  // leaves stay in Morton order: CTAs taking consecutive leaves from the counter work on
+  // siblings at the same time, so the z slices of their shared ancestors' groups are read
+  // from L2 (ncu: LPT order cost ~4% extra DRAM reads in phase 2 at 3D N=2^20)
+  (void)lbytes;
 }
 
 }  // namespace hh

@@ -114,3 +114,43 @@ def oracle_build(P, cfg, pset=None, s=None, keep_exact=False):
 
 def rel2(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b)) if np.linalg.norm(b) else float(np.linalg.norm(a))
+
+
+def _hh():
+    from paper_2604_09147_b200 import hh
+    return hh
+
+
+def leaf_blocks(B, lay, tr, R):
+    """Blocks whose target cluster contains leaf R (every level), in canonical order."""
+    d, L = tr.d, tr.L
+    lv = B["level"].astype(np.int64)
+    return np.nonzero((B["tgt"] == (np.int64(R) >> (d * (L - lv)))) & ((B["storage"] == 1) | (B["rank"] > 0)))[0]
+
+
+def oracle_leaf_rows(H, B, lay, tr, R, xt):
+    """Alg. 3 restricted to the rows of leaf R, on factors decoded with the oracle's packing
+    function from ranged arena exports.  xt: x in tree order (N, nrhs)."""
+    r0, r1 = int(tr.leaf_start[R]), int(tr.leaf_start[R + 1])
+    nr = r1 - r0
+    y = np.zeros((nr, xt.shape[1]))
+    for b in leaf_blocks(B, lay, tr, R):
+        j0, nn = int(lay["j0"][b]), int(lay["n"][b])
+        if B["storage"][b] == 1:                       # dense (fp64)
+            i0, mm = int(lay["i0"][b]), int(lay["m"][b])
+            off = int(lay["d_off"][b])
+            raw = _hh().export_arena(H, _hh().ARENA_D, off, mm * nn * 8)
+            Dm = F.from_storage_bytes(raw, F.FP64).reshape(nn, mm).T
+            y += Dm[r0 - i0:r1 - i0] @ xt[j0:j0 + nn]
+            continue
+        g, p = int(B["tag"][b]), int(B["rank"][b])
+        w = F.BYTES[g]
+        offs = PK.w_offsets(lay, b, g)
+        lo, hi = int(offs.min()), int(offs.max()) + w
+        raw = _hh().export_arena(H, _hh().ARENA_W + g, lo, hi - lo)
+        elem = np.stack([raw[offs - lo + k] for k in range(w)], axis=-1).reshape(-1)
+        Wb = F.from_storage_bytes(elem, g).reshape(nn, p)
+        base = int(lay["u_leaf_off"][g, R]) + int(lay["ucol"][b]) * nr * w
+        Ub = F.from_storage_bytes(_hh().export_arena(H, _hh().ARENA_U + g, base, nr * p * w), g).reshape(p, nr).T
+        y += Ub @ (Wb.T @ xt[j0:j0 + nn])
+    return y

@@ -100,11 +100,21 @@ def test_global_error_thm42(built):
 
 
 def test_determinism_bitwise(built):
+    """No atomics in the arithmetic, fixed summation orders: bitwise-identical y across runs,
+    across streams and for the same column inside different nrhs chunks' widths."""
     _, cfg, P, H, ex, Ho = built
     x = W.make_rhs(cfg, 2)
     y1 = PL.gpu_matvec(H, x)
     y2 = PL.gpu_matvec(H, x)
     assert np.array_equal(y1, y2)
+    s = torch.cuda.Stream()
+    xd = torch.from_numpy(x.T.copy()).cuda().T
+    yd = torch.empty_like(xd.T).T
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        hh.hh_matvec(H, xd, yd, 2, stream=s)
+    s.synchronize()
+    assert np.array_equal(yd.cpu().numpy(), y1)
 
 
 def test_rounding_routines_match_oracle():
