@@ -214,7 +214,16 @@ def stored_split(ex):
     w_bytes = int(np.sum((p * n * wb)[lr]))
     u_bytes = int(np.sum((p * m * wb)[lr]))
     d_bytes = int(np.sum((m * n * 8)[~lr]))
-    return w_bytes, u_bytes, d_bytes
+    w_elems = int(np.sum((p * n)[lr]))
+    u_elems = int(np.sum((p * m)[lr])) + int(np.sum((m * n)[~lr]))
+    return w_bytes, u_bytes, d_bytes, w_elems, u_elems
+
+
+def fp64_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+    except (OSError, ValueError):
+        return {}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -236,7 +245,7 @@ def run_ours(args, rank, world, local_rank):
     del P
     info = hh.hh_info(H)
     ex = hh.hh_export(H, tables=True, arenas=False)
-    w_bytes, u_bytes, d_bytes = stored_split(ex)
+    w_bytes, u_bytes, d_bytes, w_elems, u_elems = stored_split(ex)
     del ex
     stored = info["stored_bytes"]
     x_h = W.make_rhs(cfg, nrhs)
@@ -310,21 +319,45 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_src = (hbm, "measured (MEASURED_PEAKS.json hbm_gbs)") if hbm else (6650.0, "fallback (B200_PROFILING.md)")
     p1_ms = phase_ms[1] / max(1, nchunks)
     p2_ms = phase_ms[2] / max(1, nchunks)
-    kernels = {"phase1": (w_bytes, p1_ms), "phase2": (u_bytes + d_bytes, p2_ms)}
-    dom = max(kernels, key=lambda k: kernels[k][1])
-    alg_bytes, kms = kernels[dom]
-    achieved = alg_bytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+    kernels = {"phase1": (w_bytes, w_elems, p1_ms), "phase2": (u_bytes + d_bytes, u_elems, p2_ms)}
+    dom = max(kernels, key=lambda k: kernels[k][2])
+    alg_bytes, alg_elems, kms = kernels[dom]
+    # roofline: 2 * nrhs flops per stored element; the kernel is compute-bound when that
+    # intensity exceeds the ridge (FP64 peak / HBM peak).  NR = 8, 16 run on the FP64 tensor
+    # cores (DMMA), NR = 2, 4 on the FP64 FMA pipe (DFMA); peaks measured by scripts/fp64_peak.cu.
+    fp = fp64_peaks()
+    mma = nrhs >= 8
+    fpeak = fp.get("dmma_tflops" if mma else "dfma_tflops")
+    flops = 2.0 * min(nrhs, 16) * alg_elems
+    compute_bound = fpeak is not None and flops / max(1, alg_bytes) > fpeak * 1e3 / peak
     traffic = None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tj.get(args.config, {}).get(dom)
+        traffic = tj.get(args.config if nrhs == 1 else f"{args.config}_nrhs{nrhs}", {}).get(dom)
     except Exception:
         pass
+    if compute_bound:
+        achieved = flops / (kms / 1e3) / 1e12 if kms > 0 else 0.0
+        roof = {"bound": "tensor" if mma else "alu", "kernel": f"k_phase{dom[-1]}", "achieved": round(achieved, 2),
+                "peak": fpeak, "peak_source": "measured FP64 " + ("DMMA" if mma else "DFMA") +
+                " (profiles/fp64_peak.json, scripts/fp64_peak.cu)", "unit": "TFLOP/s",
+                "frac": round(achieved / fpeak, 4), "traffic": traffic, "algorithmic_flops_per_launch": flops,
+                "algorithmic_bytes_per_launch": alg_bytes}
+    else:
+        achieved = alg_bytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+        roof = {"bound": "hbm", "kernel": f"k_phase{dom[-1]}", "achieved": round(achieved, 1), "peak": peak,
+                "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": alg_bytes}
+    roof.update({"phase_ms_per_step": {"gather": round(phase_ms[0] / max(1, nchunks), 4), "phase1": round(p1_ms, 4),
+                                       "phase2": round(p2_ms, 4)},
+                 "phase1_GBps": round(w_bytes / (p1_ms / 1e3) / 1e9, 1) if p1_ms else None,
+                 "phase2_GBps": round((u_bytes + d_bytes) / (p2_ms / 1e3) / 1e9, 1) if p2_ms else None})
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(per_step, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "matvecs_per_s": round(world * args.steps / (ms / 1e3), 3),
+        "rhs_columns_per_s": round(world * args.steps * nrhs / (ms / 1e3), 3),
         "config": {"workload": args.config, "N": cfg["N"], "d": cfg["d"], "kernel": W.KERNEL_NAMES[cfg["kernel"]],
                    "eps": cfg["eps"], "eta": cfg["eta"], "leaf_size": cfg["leaf"], "switch_level": cfg["s"],
                    "precision_set": cfg["pset"], "nrhs": nrhs, "parallelism": f"replicas{world}",
@@ -334,13 +367,7 @@ def run_ours(args, rank, world, local_rank):
                    "l2_policy": "flush (2x L2 write) before each step" if flush else "inputs larger than L2",
                    "build_seconds": round(build_s, 2)},
         "frac_of_hbm_peak": round(value / world / peak, 4),
-        "roofline": {"bound": "hbm", "kernel": f"k_phase{dom[-1]}", "achieved": round(achieved, 1),
-                     "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
-                     "phase_ms_per_step": {"gather": round(phase_ms[0] / max(1, nchunks), 4),
-                                           "phase1": round(p1_ms, 4), "phase2": round(p2_ms, 4)},
-                     "phase1_GBps": round(w_bytes / (p1_ms / 1e3) / 1e9, 1) if p1_ms else None,
-                     "phase2_GBps": round((u_bytes + d_bytes) / (p2_ms / 1e3) / 1e9, 1) if p2_ms else None},
+        "roofline": roof,
         "e2e": e2e,
         "storage_ratio": storage_ratio("sweep" if args.config == "sweep" else args.config, stored),
         "paper_context": PAPER_CONTEXT,

@@ -96,7 +96,8 @@ enum { HH_STORE_LR = 0, HH_STORE_DENSE = 1 };
  *   precision_set bitmask of HH_P_*, must contain HH_P_FP64; may OR HH_LEDGER_ONLY.
  *   cuda_stream   cudaStream_t (NULL = legacy default stream).  hh_build synchronises it.
  *   out           receives the handle on HH_OK (unchanged otherwise).
- * Errors: HH_EINVAL (bad argument), HH_ENUMERIC (non-finite point or kernel entry, e.g.
+ * Errors: HH_EUNSUPPORTED if a block's truncated-SVD rank needs a sketch wider than 4096
+ * columns (the device compressor's limit), HH_EINVAL (bad argument), HH_ENUMERIC (non-finite point or kernel entry, e.g.
  * log of a zero distance between distinct points is mapped to 0 and counted — not an
  * error — but an overflowing entry is), HH_EDEPTH, HH_ENOMEM (arenas exceed free HBM),
  * HH_ECUDA.

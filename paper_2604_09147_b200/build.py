@@ -16,7 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libhh.so")
-SOURCES = ["api.cu", "tree.cu", "partition.cpp", "compress.cu", "dense.cu", "layout.cpp", "matvec.cu"]
+SOURCES = ["api.cu", "tree.cu", "partition.cpp", "compress.cu", "compress_big.cu", "dense.cu", "layout.cpp",
+           "matvec.cu"]
 HEADERS = ["common.cuh", "handle.h", "build.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -60,7 +61,8 @@ def build(force: bool = False, verbose_ptxas: bool = False, variant: str | None 
             if log:
                 print(log, file=sys.stderr)
     if force or not os.path.exists(lib) or any(os.path.getmtime(o) > os.path.getmtime(lib) for o in objs):
-        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs, "-lcudart"]
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs, "-lcudart", "-lcublas",
+               "-lcusolver"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -22,7 +22,7 @@ hh_status fail(hh_status s, const std::string &m) {
   return s;
 }
 
-constexpr int KMAX = 512;
+constexpr int KMAX = 4096;  // sketch width limit (HODLR-level blocks at eps=1e-6 reach ranks of ~10^3)
 
 __global__ void k_round(const double *in, int64_t n, int tag, uint32_t *out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -42,7 +42,33 @@ size_t workspace_budget() {
   return std::max<size_t>(std::min<size_t>(b, (size_t)24 << 30), (size_t)256 << 20);
 }
 
-void compress_all(hh_matrix *H, const double *pts, const std::vector<int64_t> &lr, cudaStream_t st) {
+// Runs jobs through the batched path (compress.cu) or, one by one, the whole-GPU path for
+// large wide-sketch blocks (compress_big.cu); results in job order.
+void compress_jobs(hh_matrix *H, const double *pts, const std::vector<CompressJob> &jobs, bool write, const Arenas *ar,
+                   std::vector<CompressResult> &res, cudaStream_t st, BigCtx &big) {
+  res.assign(jobs.size(), CompressResult{});
+  std::vector<CompressJob> small;
+  std::vector<size_t> small_idx;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const int64_t b = jobs[i].block;
+    int64_t i0, m, j0, n;
+    cluster_range(H, H->level[b], H->tgt[b], i0, m);
+    cluster_range(H, H->level[b], H->src[b], j0, n);
+    if (use_big_path(m, n, jobs[i].k)) {
+      run_compress_big(H, pts, jobs[i], write, ar, res[i], st, big);
+    } else {
+      small.push_back(jobs[i]);
+      small_idx.push_back(i);
+    }
+  }
+  if (!small.empty()) {
+    std::vector<CompressResult> rs;
+    run_compress(H, pts, small, write, ar, rs, st, workspace_budget());
+    for (size_t i = 0; i < small.size(); ++i) res[small_idx[i]] = rs[i];
+  }
+}
+
+void compress_all(hh_matrix *H, const double *pts, const std::vector<int64_t> &lr, cudaStream_t st, BigCtx &big) {
   // pass 1 with adaptive sketch width: k0 per (level, kind) class from the ranks seen so far
   const size_t nb = H->level.size();
   H->rank.assign(nb, 0);
@@ -69,21 +95,22 @@ void compress_all(hh_matrix *H, const double *pts, const std::vector<int64_t> &l
       }
       pos = end;
     }
-    run_compress(H, pts, jobs, false, nullptr, res, st, workspace_budget());
+    compress_jobs(H, pts, jobs, false, nullptr, res, st, big);
     for (size_t i = 0; i < jobs.size(); ++i) {
       const int64_t b = jobs[i].block;
       const CompressResult &r = res[i];
-      const int sh = H->d * (H->L - H->level[b]);
-      const int64_t m = H->leaf_start[(H->tgt[b] + 1) << sh] - H->leaf_start[H->tgt[b] << sh];
-      const int64_t n = H->leaf_start[(H->src[b] + 1) << sh] - H->leaf_start[H->src[b] << sh];
+      int64_t i0, m, j0, n;
+      cluster_range(H, H->level[b], H->tgt[b], i0, m);
+      cluster_range(H, H->level[b], H->src[b], j0, n);
       const int kfull = (int)std::min<int64_t>(std::min(m, n), KMAX);
       if (!r.ok && r.k < kfull) {
-        const int kn = r.k < 64 ? 2 * r.k : ((r.k + r.k / 2 + 7) / 8) * 8;
+        // widen the sketch: x2 while small or on the whole-GPU path, then x1.5
+        const int kn = (r.k < 64 || use_big_path(m, n, r.k)) ? 2 * r.k : ((r.k + r.k / 2 + 7) / 8) * 8;
         retry.push_back(CompressJob{b, std::min(kfull, kn)});
         ++retries;
         continue;
       }
-      HH_REQUIRE(r.p >= 0, HH_EUNSUPPORTED, "block rank exceeds the sketch limit (512)");
+      HH_REQUIRE(r.p >= 0, HH_EUNSUPPORTED, "block rank exceeds the sketch limit (4096)");
       HH_REQUIRE(std::isfinite(r.tot) && std::isfinite(r.nb2), HH_ENUMERIC, "non-finite kernel entry");
       H->rank[b] = r.p;
       H->kfinal[b] = r.k;
@@ -167,7 +194,8 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
         lr.push_back((int64_t)b);
       }
     }
-    compress_all(H, pts.as<double>(), lr, st);                         // a3 (pass 1)
+    BigCtx big;
+    compress_all(H, pts.as<double>(), lr, st, big);                    // a3 (pass 1)
     run_dense(H, pts.as<double>(), dn, false, st);                    // dense norms
     for (size_t b = 0; b < nb; ++b)
       HH_REQUIRE(std::isfinite(H->tot[b]), HH_ENUMERIC, "non-finite kernel entry");
@@ -202,7 +230,7 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
       for (size_t b = 0; b < nb; ++b)
         if (H->storage[b] == STORE_LR && H->rank[b] > 0) jobs.push_back(CompressJob{(int64_t)b, H->kfinal[b]});
       std::vector<CompressResult> res;
-      run_compress(H, pts.as<double>(), jobs, true, &ar, res, st, workspace_budget());
+      compress_jobs(H, pts.as<double>(), jobs, true, &ar, res, st, big);
       // pass 2 writes the factors of the pass-1 rank; its maxabs must reproduce pass 1's
       // (the range guard decided the tags from it): a cheap determinism check
       int64_t mism = 0;

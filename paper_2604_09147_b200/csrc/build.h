@@ -27,6 +27,20 @@ struct Arenas {
   int64_t ncell;
 };
 
+// Whole-GPU compression of one large, wide-sketch block (compress_big.cu): cuBLAS/cuSOLVER
+// handles and workspaces kept across the blocks of one hh_build.
+struct BigCtx {
+  struct Impl;
+  Impl *p;
+  BigCtx();
+  ~BigCtx();
+  BigCtx(const BigCtx &) = delete;
+  BigCtx &operator=(const BigCtx &) = delete;
+};
+bool use_big_path(int64_t m, int64_t n, int k);
+void run_compress_big(hh_matrix *H, const double *pts, const CompressJob &job, bool write, const Arenas *ar,
+                      CompressResult &res, cudaStream_t st, BigCtx &ctx);
+
 KernelFn make_kernel_fn(const hh_kernel &kk);
 void build_tree(hh_matrix *H, const double *P, cudaStream_t st, DBuf &pts_tree);
 void build_partition(hh_matrix *H);

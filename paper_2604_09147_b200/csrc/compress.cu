@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(THREADS) k_gemm_gen(const Task *__restrict__ t
   const int k = B.k;
   const int c0 = blockIdx.y * GT_N;
   if (c0 >= k) return;
-  __shared__ double As[GT_K][GT_M + 1];
-  __shared__ double Xs[GT_K][GT_N + 1];
+  __shared__ __align__(16) double As[GT_K][GT_M + 2];  // +2: 16-B aligned rows for 128-bit loads
+  __shared__ __align__(16) double Xs[GT_K][GT_N + 2];
   __shared__ double rp[3][GT_M];
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;  // 16 x 16 threads, 4 x 4 outputs each
@@ -143,9 +143,17 @@ __global__ void __launch_bounds__(THREADS) k_gemm_gen(const Task *__restrict__ t
     for (int jj = 0; jj < GT_K; ++jj) {
       double a[4], x[TC];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) a[q] = As[jj][ty * 4 + q];
+      for (int q = 0; q < 4; q += 2) {
+        const double2 t = *reinterpret_cast<const double2 *>(&As[jj][ty * 4 + q]);
+        a[q] = t.x;
+        a[q + 1] = t.y;
+      }
 #pragma unroll
-      for (int q = 0; q < TC; ++q) x[q] = Xs[jj][tx * TC + q];
+      for (int q = 0; q < TC; q += 2) {
+        const double2 t = *reinterpret_cast<const double2 *>(&Xs[jj][tx * TC + q]);
+        x[q] = t.x;
+        x[q + 1] = t.y;
+      }
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll

@@ -57,10 +57,12 @@ constexpr int META = 64;
 #endif
 template <int NR> constexpr bool use_mma() { return HH_MV_MMA && (NR == 8 || NR == 16); }
 
-template <int NR> struct Geo {
+template <int NR, int PH> struct Geo {  // PH = phase (1: x~ rows per W row window, 2: z per U column)
   static constexpr int WDATA = HH_MV_WDATA;                       // factor bytes per stage
   static constexpr int WBUF = WDATA + 32;                            // + 16-B alignment slack
-  static constexpr int XDATA = NR <= 2 ? HH_MV_XDATA : NR * 2048;  // vector bytes per stage
+  // vector bytes per stage: phase 1 needs one NR-vector per W row (a 248-column row is >= 1 KiB
+  // of factors), phase 2 one per U column (|R| rows, as little as ~32 elements)
+  static constexpr int XDATA = NR <= 2 ? HH_MV_XDATA : (PH == 1 ? (NR * 512 > 4096 ? NR * 512 : 4096) : NR * 2048);
   static constexpr int XELEMS = XDATA / 8;                        // doubles (rows x NR)
   static constexpr int XBUF = XDATA + 32;
   static constexpr int STAGE = WBUF + XBUF + META;
@@ -330,7 +332,7 @@ __device__ __forceinline__ void p1_mma_consumer(const P1Args &a, uint8_t *smem, 
 
 template <int NR>
 __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
-  using G = Geo<NR>;
+  using G = Geo<NR, 1>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
   uint64_t *empty = full + G::STAGES;
@@ -555,22 +557,22 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
           c[mt][nt][0] = c[mt][nt][1] = 0.0;
         }
       consumer_sync();
-      if (warp < MG) {  // ks == 0 warp of group mg: fixed-order sum over k-slices
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          const int r = mg * 32 + mt * 8 + (lane >> 2);
-          if (r >= nr) continue;
-          const int64_t i = a.perm[m.p + r];
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              double sum = 0.0;
-              for (int k = 0; k < KS; ++k)
-                sum += red[(size_t)(mg + k * MG) * 4 * NT * 64 + ((mt * NT + nt) * 32 + lane) * 2 + h];
-              a.y[i + (int64_t)(nt * 8 + 2 * (lane & 3) + h) * a.ldy] = sum;
-            }
+      // every warp finalises some of the MG x 4 x NT output fragments: fixed-order sum over
+      // the KS k-slices, then the scatter y[perm[t]] (a10)
+      for (int f = warp; f < MG * 4 * NT; f += NCW) {
+        const int g = f / (4 * NT), mt = (f / NT) % 4, nt = f % NT;
+        const int r = g * 32 + mt * 8 + (lane >> 2);
+        if (r >= nr) continue;
+        double s0 = 0.0, s1 = 0.0;
+        for (int k = 0; k < KS; ++k) {
+          const double *src = red + (size_t)(g + k * MG) * 4 * NT * 64 + ((mt * NT + nt) * 32 + lane) * 2;
+          s0 += src[0];
+          s1 += src[1];
         }
+        const int64_t i = a.perm[m.p + r];
+        const int64_t col = nt * 8 + 2 * (lane & 3);
+        a.y[i + col * a.ldy] = s0;
+        a.y[i + (col + 1) * a.ldy] = s1;
       }
       consumer_sync();
       kbase = 0;
@@ -580,7 +582,7 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
 
 template <int NR>
 __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
-  using G = Geo<NR>;
+  using G = Geo<NR, 2>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
   uint64_t *empty = full + G::STAGES;
@@ -731,7 +733,8 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
 template <int NR>
 void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
   using namespace mv;
-  using G = Geo<NR>;
+  using G1 = Geo<NR, 1>;
+  using G2 = Geo<NR, 2>;
   int dev = 0, nsm = 148;
   HH_CUDA(cudaGetDevice(&dev));
   HH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -759,7 +762,7 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     a.v = v;
     a.N = H->N;
     a.ctr = ctr;
-    const size_t sm = G::smem(false);
+    const size_t sm = G1::smem(false);
     static bool attr1[17] = {};
     if (!attr1[NR]) {
       HH_CUDA(cudaFuncSetAttribute(k_phase1<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -784,7 +787,7 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   b.y = y + (int64_t)col0 * H->N;
   b.ldy = H->N;
   b.ctr = ctr;
-  const size_t sm2 = G::smem(true);
+  const size_t sm2 = G2::smem(true);
   static bool attr2[17] = {};
   if (!attr2[NR]) {
     HH_CUDA(cudaFuncSetAttribute(k_phase2<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));

@@ -1,4 +1,6 @@
 """GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.  Needs a B200."""
+import os
+
 import numpy as np
 import pytest
 
@@ -17,6 +19,7 @@ if not torch.cuda.is_available():
 import parity_lib as PL  # noqa: E402
 from paper_2604_09147_b200 import hh  # noqa: E402
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SMALL = ["2d_tiny", "2d_fig8_e4", "2d_fig8_e2", "3d_small_inv_r", "3d_small_exp"]
 
 
@@ -173,3 +176,33 @@ def test_invalid_arguments_are_rejected():
     with pytest.raises(hh.HHError) as e:
         hh.hh_build(bad, 0, 1.0, 1e-6, 1.0, 16, 2, W.P_MIXED)
     assert e.value.status == hh.HH_ENUMERIC
+
+
+def test_whole_gpu_compression_path_matches_oracle():
+    """compress_big.cu (explicit entries + cuBLAS/cuSOLVER, used for large wide-sketch blocks)
+    gives the same partition, ranks, tags and matvec as the oracle; forced onto every block of
+    a small 3D problem with HH_BIG_FLOPS (read by the library at its first use in this process)."""
+    import subprocess
+    import sys
+    code = r'''
+import os, sys
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+import numpy as np, workloads as W, parity_lib as PL
+cfg = dict(W.SMALL_CONFIGS["3d_small_inv_r"], s=0)
+P = W.make_points(cfg)
+H = PL.gpu_build(P, cfg)
+ex = PL.export(H)
+Ho = PL.oracle_build(P, cfg)
+PL.check_partition(ex, Ho)
+bad_r, bad_t, st = PL.rank_tag_parity(ex, Ho)
+assert bad_r == 0 and bad_t == 0, st
+lay = PL.check_packing(ex)
+x = W.make_rhs(cfg, 3)
+r = PL.rel2(PL.gpu_matvec(H, x), PL.oracle_matvec_on_export(ex, lay, x))
+assert r <= 1e-12, r
+print("big-path ok", st, r)
+'''
+    env = dict(os.environ, HH_BIG_FLOPS="1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "big-path ok" in out.stdout
