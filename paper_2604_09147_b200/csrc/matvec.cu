@@ -45,6 +45,9 @@ constexpr int THREADS = NCT + 32;      // + one producer warp
 #ifndef HH_MV_XDATA
 #define HH_MV_XDATA 4096
 #endif
+#ifndef HH_MV_P2HI
+#define HH_MV_P2HI 32768
+#endif
 #ifndef HH_MV_STAGES
 #define HH_MV_STAGES 2
 #endif
@@ -58,11 +61,13 @@ constexpr int META = 64;
 template <int NR> constexpr bool use_mma() { return HH_MV_MMA && (NR == 8 || NR == 16); }
 
 template <int NR, int PH> struct Geo {  // PH = phase (1: x~ rows per W row window, 2: z per U column)
-  static constexpr int WDATA = HH_MV_WDATA;                       // factor bytes per stage
+  // factor bytes per stage (phase 2 at NR >= 8 may use smaller stages to fit 2 CTAs/SM)
+  static constexpr int WDATA = (PH == 2 && NR >= 8) ? HH_MV_P2HI : HH_MV_WDATA;
   static constexpr int WBUF = WDATA + 32;                            // + 16-B alignment slack
   // vector bytes per stage: phase 1 needs one NR-vector per W row (a 248-column row is >= 1 KiB
   // of factors), phase 2 one per U column (|R| rows, as little as ~32 elements)
-  static constexpr int XDATA = NR <= 2 ? HH_MV_XDATA : (PH == 1 ? (NR * 512 > 4096 ? NR * 512 : 4096) : NR * 2048);
+  static constexpr int XDATA =
+      NR <= 2 ? HH_MV_XDATA : (PH == 1 ? (NR * 512 > 4096 ? NR * 512 : 4096) : NR * 2048 / (32768 / WDATA));
   static constexpr int XELEMS = XDATA / 8;                        // doubles (rows x NR)
   static constexpr int XBUF = XDATA + 32;
   static constexpr int STAGE = WBUF + XBUF + META;
