@@ -46,7 +46,7 @@ constexpr int THREADS = NCT + 32;      // + one producer warp
 #define HH_MV_XDATA 4096
 #endif
 #ifndef HH_MV_P2HI
-#define HH_MV_P2HI 32768
+#define HH_MV_P2HI 16384   // phase 2 at NR = 16: 16 KiB stages fit 2 CTAs/SM (measured faster)
 #endif
 #ifndef HH_MV_STAGES
 #define HH_MV_STAGES 2
@@ -62,7 +62,7 @@ template <int NR> constexpr bool use_mma() { return HH_MV_MMA && (NR == 8 || NR 
 
 template <int NR, int PH> struct Geo {  // PH = phase (1: x~ rows per W row window, 2: z per U column)
   // factor bytes per stage (phase 2 at NR >= 8 may use smaller stages to fit 2 CTAs/SM)
-  static constexpr int WDATA = (PH == 2 && NR >= 8) ? HH_MV_P2HI : HH_MV_WDATA;
+  static constexpr int WDATA = (PH == 2 && NR >= 16) ? HH_MV_P2HI : HH_MV_WDATA;
   static constexpr int WBUF = WDATA + 32;                            // + 16-B alignment slack
   // vector bytes per stage: phase 1 needs one NR-vector per W row (a 248-column row is >= 1 KiB
   // of factors), phase 2 one per U column (|R| rows, as little as ~32 elements)
@@ -191,7 +191,7 @@ __device__ __forceinline__ double up(const typename Elem<TAG>::T v) {
 // D = A B + D on the FP64 tensor cores: A 8x4 (thread holds A[lane/4][lane%4]), B 4x8
 // (thread holds B[lane%4][lane/4]), C/D 8x8 (thread holds row lane/4, columns 2(lane%4)+{0,1}).
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
