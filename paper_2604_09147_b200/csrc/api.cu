@@ -244,11 +244,17 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
       // matvec plan + workspace
       std::vector<P1Tile> tiles;
       std::vector<int32_t> zmap;
+      std::vector<P1Combine> comb;
       std::vector<P2Seg> segs;
       std::vector<P2Leaf> leaves;
-      build_plan(H, tiles, zmap, segs, leaves);
+      int64_t npartial = 0;
+      build_plan(H, tiles, zmap, comb, npartial, segs, leaves);
       h2d(H->p1_tiles, tiles, st);
       h2d(H->zmap, zmap, st);
+      h2d(H->p1_comb, comb, st);
+      H->n_p1_comb = (int64_t)comb.size();
+      H->n_partial = npartial;
+      H->partial.alloc(sizeof(double) * 16 * (size_t)std::max<int64_t>(1, npartial));
       h2d(H->p2_segs, segs, st);
       h2d(H->p2_leaves, leaves, st);
       H->n_p1_tiles = (int64_t)tiles.size();

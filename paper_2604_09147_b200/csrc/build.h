@@ -50,8 +50,8 @@ void run_dense(hh_matrix *H, const double *pts, const std::vector<int64_t> &bloc
 void assign_tags(hh_matrix *H);
 void compute_layout(hh_matrix *H);
 void cluster_range(const hh_matrix *H, int l, int64_t m, int64_t &a, int64_t &n);
-void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &zmap, std::vector<P2Seg> &segs,
-                std::vector<P2Leaf> &leaves);
+void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &zmap, std::vector<P1Combine> &comb,
+                int64_t &npartial, std::vector<P2Seg> &segs, std::vector<P2Leaf> &leaves);
 void run_matvec(hh_matrix *H, const double *x, double *y, int nrhs, cudaStream_t st);
 void print_build_profile();
 

@@ -41,14 +41,24 @@ template <class T> void h2d(DBuf &b, const std::vector<T> &v, cudaStream_t s) {
 // into column tiles of width <= W_CT, each stored row-major and 16-B aligned.
 constexpr int W_CT = 248;  // row stride = 24 (fp32) / 28 (16-bit) banks mod 32: conflict-free 4-row DMMA fragments
 
-// Phase-1 work item: one column tile of one W panel (all |J| rows).
+// Phase-1 work item: a row range of one column tile of one W panel.  Tiles taller than
+// P1_ROWS are cut into row pieces whose partial column sums go to a workspace and are added
+// in piece order by a combine pass (load balance for HODLR-level panels).
+constexpr int P1_ROWS = 4096;
 struct P1Tile {
   int64_t src;        // byte offset of the tile in W[tag] (multiple of 16)
-  int64_t x0;         // v index (tree position) of the panel's row 0
+  int64_t x0;         // v index (tree position) of the tile's row 0
   int64_t zbase;      // index into zmap of the tile's column 0
-  int32_t n;          // rows (= |J|)
+  int64_t pbase;      // -1: write z; else partial index of column 0 of this piece
+  int32_t n;          // rows of this piece
+  int32_t r0;         // first row of this piece inside the tile
   int16_t ct;         // columns (1..W_CT)
   int16_t tag;
+  int32_t pad;
+};
+struct P1Combine {    // z[zmap[zbase + c]] = sum_{q < npieces} partial[pbase + q * ct + c]
+  int64_t zbase, pbase;
+  int32_t ct, npieces;
 };
 // Phase-2 work: per leaf R, a list of segments; a segment is `ncols` contiguous |R|-row
 // columns (column-major) of U[tag] or of the dense arena, multiplied by v[vbeg ...].
@@ -95,8 +105,8 @@ struct hh_matrix {
   hh::DBuf W[4], U[4], D;
   int64_t w_bytes[4] = {0, 0, 0, 0}, u_bytes[4] = {0, 0, 0, 0}, d_bytes = 0;
   // matvec plan
-  hh::DBuf p1_tiles, zmap, p2_segs, p2_leaves;
-  int64_t n_p1_tiles = 0, n_p2_leaves = 0;
+  hh::DBuf p1_tiles, zmap, p2_segs, p2_leaves, p1_comb, partial;
+  int64_t n_p1_tiles = 0, n_p2_leaves = 0, n_p1_comb = 0, n_partial = 0;
   hh::DBuf v;        // [(N + ztotal) * 16] doubles (+ slack for 16-B aligned superset copies)
   hh::DBuf ctr;      // work counters of the persistent matvec kernels (zeroed by the gather)
   hh::DBuf hx, hy;   // staging for hh_matvec_host

@@ -11,6 +11,7 @@
 //       independently; check (1c) compares them bit for bit.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <vector>
 
@@ -246,13 +247,15 @@ void compute_layout(hh_matrix *H) {
 // counter, so big tiles start early).  zmap[zbase + c] = z index of tile column c.
 // Phase 2: per leaf, dense segments then per tag the levels' U column groups; leaves in
 // Morton order.
-void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &zmap, std::vector<P2Seg> &segs,
-                std::vector<P2Leaf> &leaves) {
+void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &zmap, std::vector<P1Combine> &comb,
+                int64_t &npartial, std::vector<P2Seg> &segs, std::vector<P2Leaf> &leaves) {
   const size_t nb = H->level.size();
   const int d = H->d, L = H->L;
   const int64_t N = H->N;
   tiles.clear();
   zmap.clear();
+  comb.clear();
+  npartial = 0;
   segs.clear();
   leaves.clear();
   HH_REQUIRE(H->ztotal < INT32_MAX, HH_EUNSUPPORTED, "total rank exceeds 2^31");
@@ -266,6 +269,8 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
     return H->wcol[a] < H->wcol[c];
   });
   std::vector<int64_t> tbytes;
+  // row-split threshold (HH_P1_ROWS lowers it so tests exercise the split on small inputs)
+  static const int64_t split_rows = getenv("HH_P1_ROWS") ? std::max(1ll, atoll(getenv("HH_P1_ROWS"))) : P1_ROWS;
   size_t i = 0;
   while (i < idx.size()) {
     size_t e = i;
@@ -283,8 +288,20 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
     int64_t off = H->w_off[b0];
     for (int64_t c0 = 0; c0 < P; c0 += W_CT) {
       const int64_t ct = std::min<int64_t>(W_CT, P - c0);
-      tiles.push_back(P1Tile{off, j0, (int64_t)zmap.size(), (int32_t)n, (int16_t)ct, (int16_t)g});
-      tbytes.push_back(n * ct * tag_bytes(g));
+      const int64_t zb = (int64_t)zmap.size();
+      if (n <= split_rows) {
+        tiles.push_back(P1Tile{off, j0, zb, -1, (int32_t)n, 0, (int16_t)ct, (int16_t)g, 0});
+        tbytes.push_back(n * ct * tag_bytes(g));
+      } else {
+        const int32_t np = (int32_t)((n + split_rows - 1) / split_rows);
+        comb.push_back(P1Combine{zb, npartial, (int32_t)ct, np});
+        for (int32_t q = 0; q < np; ++q) {
+          const int64_t r0 = (int64_t)q * split_rows, rn = std::min<int64_t>(split_rows, n - r0);
+          tiles.push_back(P1Tile{off, j0, zb, npartial + q * ct, (int32_t)rn, (int32_t)r0, (int16_t)ct, (int16_t)g, 0});
+          tbytes.push_back(rn * ct * tag_bytes(g));
+        }
+        npartial += (int64_t)np * ct;
+      }
       zmap.insert(zmap.end(), pz.begin() + c0, pz.begin() + c0 + ct);
       off += align_up(n * ct * tag_bytes(g));
     }

@@ -88,7 +88,8 @@ struct Meta {
   int32_t r0, r1;    // phase 1: rows [r0, r1) of the tile;  phase 2: columns [r0, r1) of the segment
   int32_t flags;     // phase 2: bit 0 = last stage of the leaf
   int32_t a, b;      // phase 1: ct, tag;  phase 2: nr, tag | dense << 8
-  int64_t p, q;      // phase 1: zbase, n;  phase 2: leaf r0, -
+  int64_t p, q;      // phase 1: zbase, rows of the piece;  phase 2: leaf r0, -
+  int64_t pb;        // phase 1: partial index of column 0 (row-split tile) or -1
 };
 static_assert(sizeof(Meta) <= META, "meta");
 
@@ -208,10 +209,31 @@ __global__ void k_gather(const int32_t *__restrict__ perm, const double *__restr
   }
 }
 
+// a8 (second pass for row-split tiles): z = sum over pieces in piece order (deterministic)
+template <int NR>
+__global__ void k_p1_combine(const P1Combine *__restrict__ cm, int64_t ncomb, const int32_t *__restrict__ zmap,
+                             const double *__restrict__ partial, double *v, int64_t N) {
+  for (int64_t t = blockIdx.x; t < ncomb; t += gridDim.x) {
+    const P1Combine C = cm[t];
+    for (int c = threadIdx.x; c < C.ct; c += blockDim.x) {
+      double s[NR];
+#pragma unroll
+      for (int k = 0; k < NR; ++k) s[k] = 0.0;
+      for (int q = 0; q < C.npieces; ++q)
+#pragma unroll
+        for (int k = 0; k < NR; ++k) s[k] += partial[(C.pbase + (int64_t)q * C.ct + c) * NR + k];
+      double *out = v + (N + zmap[C.zbase + c]) * NR;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) out[k] = s[k];
+    }
+  }
+}
+
 // --------------------------------------------------------------------------- phase 1
 struct P1Args {
   const P1Tile *tiles;
   const int32_t *zmap;
+  double *partial;    // [npartial] x NR partial column sums of row-split tiles
   int64_t ntiles;
   const uint8_t *W[4];
   double *v;          // [x~ (N) ; z] x NR
@@ -304,7 +326,7 @@ __device__ __forceinline__ void p1_mma_consumer(const P1Args &a, uint8_t *smem, 
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
         const int col = col0 + mt * 8 + (lane >> 2);
-        if (col < ct) zi[mt] = a.zmap[m.p + col];
+        if (col < ct && m.pb < 0) zi[mt] = a.zmap[m.p + col];
       }
     }
     if (active) {
@@ -325,7 +347,7 @@ __device__ __forceinline__ void p1_mma_consumer(const P1Args &a, uint8_t *smem, 
       for (int mt = 0; mt < 4; ++mt) {
         const int col = col0 + mt * 8 + (lane >> 2);
         if (col < ct) {
-          double *out = a.v + (a.N + zi[mt]) * NR + 2 * (lane & 3);
+          double *out = (m.pb >= 0 ? a.partial + (m.pb + col) * NR : a.v + (a.N + zi[mt]) * NR) + 2 * (lane & 3);
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
             *reinterpret_cast<double2 *>(out + nt * 8) = make_double2(c[mt][nt][0], c[mt][nt][1]);
@@ -361,8 +383,8 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
       const int w = tag_bytes(T.tag);
       const int rowb = T.ct * w;
       const int rs = max(1, min(G::XELEMS / NR, G::WDATA / rowb));
-      const uint8_t *wbase = pick(a.W, T.tag) + T.src;
-      const uint8_t *xbase = reinterpret_cast<const uint8_t *>(a.v + T.x0 * NR);
+      const uint8_t *wbase = pick(a.W, T.tag) + T.src + (int64_t)T.r0 * rowb;
+      const uint8_t *xbase = reinterpret_cast<const uint8_t *>(a.v + (T.x0 + T.r0) * NR);
       for (int r0 = 0; r0 < T.n; r0 += rs, ++n) {
         const int r1 = min(T.n, r0 + rs);
         const int s = n % G::STAGES;
@@ -382,6 +404,7 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
         m->b = T.tag;
         m->p = T.zbase;
         m->q = T.n;
+        m->pb = T.pbase;
         mbar_expect_tx(&full[s], window_bytes(wsrc, wlen) + window_bytes(xsrc, xlen));
         uint32_t tx = 0;
         stage_copy(st, wsrc, wlen, &full[s], pol_w, tx);
@@ -424,7 +447,7 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
       for (int b = 0; b < MB; ++b) {
 #pragma unroll
         for (int k = 0; k < NR; ++k) acc[b][k] = 0.0;
-        if (valid[b] && q == 0) zi[b] = a.zmap[m.p + cs + b * slots];
+        if (valid[b] && q == 0 && m.pb < 0) zi[b] = a.zmap[m.p + cs + b * slots];
       }
     }
     if (active) {
@@ -464,7 +487,7 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
 #pragma unroll
         for (int b = 0; b < MB; ++b)
           if (valid[b]) {
-            double *out = a.v + (a.N + zi[b]) * NR;
+            double *out = m.pb >= 0 ? a.partial + (m.pb + cs + b * slots) * NR : a.v + (a.N + zi[b]) * NR;
 #pragma unroll
             for (int k = 0; k < NR; ++k) out[k] = acc[b][k];
           }
@@ -762,6 +785,7 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     P1Args a{};
     a.tiles = H->p1_tiles.as<P1Tile>();
     a.zmap = H->zmap.as<int32_t>();
+    a.partial = H->partial.as<double>();
     a.ntiles = H->n_p1_tiles;
     for (int g = 0; g < 4; ++g) a.W[g] = H->W[g].as<uint8_t>();
     a.v = v;
@@ -778,6 +802,11 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     const int64_t grid = std::min<int64_t>(H->n_p1_tiles, (int64_t)nsm * std::max(1, per_sm));
     k_phase1<NR><<<(unsigned)grid, THREADS, sm, st>>>(a);
     HH_LAUNCHED();
+    if (H->n_p1_comb > 0) {
+      k_p1_combine<NR><<<(unsigned)std::min<int64_t>(H->n_p1_comb, (int64_t)nsm * 8), 256, 0, st>>>(
+          H->p1_comb.as<P1Combine>(), H->n_p1_comb, a.zmap, a.partial, v, H->N);
+      HH_LAUNCHED();
+    }
   }
   mark(2);
   // a9 + a10 phase 2 with fused scatter

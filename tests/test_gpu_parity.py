@@ -206,3 +206,63 @@ print("big-path ok", st, r)
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "big-path ok" in out.stdout
+
+
+def test_degenerate_sizes_and_duplicates():
+    """N = 1 and N = 2 (single leaf: the dense diagonal block, K(x,x) = 0 for singular
+    kernels and 1 for exp, PAPER.md:1119); duplicated points beyond 62 key bits -> HH_EDEPTH;
+    a duplicate pair inside a leaf is a zero entry for singular kernels (reading G18)."""
+    for kern, diag in ((W.K_INV_R, 0.0), (W.K_EXP, 1.0)):
+        P1 = np.array([[0.3, 0.4, 0.5]])
+        H = PL.gpu_build(P1, dict(kernel=kern, scale=0.1, eps=1e-6, eta=1.0, leaf=8, s=0, pset=W.P_MIXED))
+        y = PL.gpu_matvec(H, np.array([[2.0]]))
+        assert y[0, 0] == diag * 2.0
+        P2 = np.array([[0.0, 0.0, 0.0], [0.3, 0.4, 0.0]])            # distance 0.5
+        H = PL.gpu_build(P2, dict(kernel=kern, scale=0.1, eps=1e-6, eta=1.0, leaf=8, s=0, pset=W.P_MIXED))
+        y = PL.gpu_matvec(H, np.array([[1.0], [3.0]]))
+        off = 2.0 if kern == W.K_INV_R else np.exp(-5.0)
+        np.testing.assert_allclose(y[:, 0], [diag * 1.0 + off * 3.0, off * 1.0 + diag * 3.0], rtol=1e-15)
+    Pd = np.repeat(np.array([[0.25, 0.5]]), 40, axis=0)
+    with pytest.raises(hh.HHError) as e:
+        PL.gpu_build(Pd, dict(kernel=W.K_LOG, scale=1.0, eps=1e-6, eta=1.0, leaf=16, s=0, pset=W.P_MIXED))
+    assert e.value.status == hh.HH_EDEPTH
+    Pp = W.points_uniform(500, 2, 4)
+    Pp[7] = Pp[3]                                                    # coincident distinct points
+    cfg = dict(kernel=W.K_LOG, scale=1.0, eps=1e-8, eta=1.0, leaf=32, s=2, pset=W.P_MIXED)
+    H = PL.gpu_build(Pp, cfg)
+    x = W.rhs(500, 1, 5, "uniform_pm1")
+    A = D.dense_matrix(Pp, W.K_LOG, 1.0)
+    assert A[3, 7] == 0.0 and A[7, 3] == 0.0
+    assert PL.rel2(PL.gpu_matvec(H, x), A @ x) < 1e-7
+
+
+def test_row_split_phase1_matches_oracle():
+    """Phase-1 row splitting (partial column sums + fixed-order combine) forced on every W
+    tile taller than 40 rows with HH_P1_ROWS; results within 1e-12 of the oracle's Alg. 3 on
+    the exported factors, bitwise reproducible, for nrhs = 1, 3 (DFMA) and 16 (DMMA)."""
+    import subprocess
+    import sys
+    code = r'''
+import os, sys
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+import numpy as np, workloads as W, parity_lib as PL
+for name in ("2d_tiny", "3d_small_exp"):
+    cfg = W.SMALL_CONFIGS[name]
+    P = W.make_points(cfg)
+    H = PL.gpu_build(P, cfg)
+    ex = PL.export(H)
+    lay = PL.check_packing(ex)
+    for nrhs in (1, 3, 16):
+        x = W.make_rhs(cfg, nrhs)
+        y = PL.gpu_matvec(H, x)
+        assert np.array_equal(y, PL.gpu_matvec(H, x))
+        yo = PL.oracle_matvec_on_export(ex, lay, x)
+        for c in range(nrhs):
+            r = PL.rel2(y[:, c], yo[:, c])
+            assert r <= 1e-12, (name, nrhs, c, r)
+print("row-split ok")
+'''
+    env = dict(os.environ, HH_P1_ROWS="40")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "row-split ok" in out.stdout
