@@ -298,11 +298,12 @@ __global__ void __launch_bounds__(THREADS) k_qr(CBlk *blks, double *ws, int whic
 // M = T^T (k x k) where T = upper triangle of the QR of Z (stored in Zc, ld n).
 // Output: s (descending) at os, Ut (k x k, columns = left singular vectors of T^T) at ot.
 constexpr int JAC_SMEM_K = 168;   // 168^2 doubles = 220.5 KiB of shared memory
-constexpr int JT = 1024;          // Jacobi block size (32 warps -> 32 rotation pairs in flight)
-
-__global__ void __launch_bounds__(JT) k_jacobi(CBlk *blks, double *ws) {
+// JT threads per block (JT/32 rotation pairs in flight); launched per k-bucket so that small
+// cores get small CTAs and small shared memory (several blocks per SM).
+template <int JT>
+__global__ void __launch_bounds__(JT) k_jacobi(CBlk *blks, const int32_t *__restrict__ order, double *ws) {
   extern __shared__ double smem[];
-  CBlk &B = blks[blockIdx.x];
+  CBlk &B = blks[order[blockIdx.x]];
   const int k = B.k, n = B.n;
   double *M = (k <= JAC_SMEM_K) ? smem : ws + B.oy;  // Y no longer needed (Q formed)
   const double *R = ws + B.ozc;
@@ -645,7 +646,7 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
   res.assign(jobs.size(), CompressResult{});
   const KernelFn K = make_kernel_fn(H->kernel);
   const double delta = 1e-9;
-  DBuf wsb, blkb, taskb, partb;
+  DBuf wsb, blkb, taskb, partb, ordb;
   size_t ws_cap = 0;
   size_t pos = 0;
   std::vector<CBlk> blks;
@@ -749,11 +750,38 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
     k_qr<false><<<nb, THREADS, 0, st>>>(db, ws, 1);
     HH_LAUNCHED();
     mark(4);
-    const int jsm = std::min(kmax, JAC_SMEM_K);
-    const size_t jsmem = sizeof(double) * (size_t)jsm * jsm;
-    HH_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * JAC_SMEM_K * JAC_SMEM_K)));
-    k_jacobi<<<nb, JT, jsmem, st>>>(db, ws);
-    HH_LAUNCHED();
+    {
+      // k-buckets: (k <= 32: 256 threads), (<= 64: 512), (<= 168: 1024, smem), (> 168: global)
+      std::vector<int32_t> ord;
+      int cnt[4] = {0, 0, 0, 0}, kmx[4] = {0, 0, 0, 0};
+      auto bucket = [](int k) { return k <= 32 ? 0 : k <= 64 ? 1 : k <= JAC_SMEM_K ? 2 : 3; };
+      for (int bkt = 0; bkt < 4; ++bkt)
+        for (int i = 0; i < nb; ++i)
+          if (bucket(blks[i].k) == bkt) {
+            ord.push_back(i);
+            ++cnt[bkt];
+            kmx[bkt] = std::max(kmx[bkt], blks[i].k);
+          }
+      h2d(ordb, ord, st);
+      const int32_t *od = ordb.as<int32_t>();
+      int start = 0;
+      for (int bkt = 0; bkt < 4; ++bkt) {
+        if (cnt[bkt] == 0) continue;
+        const int jsm = std::min(kmx[bkt], JAC_SMEM_K);
+        const size_t jsmem = bkt == 3 ? 0 : sizeof(double) * (size_t)jsm * jsm;
+        if (bkt == 0) {
+          k_jacobi<256><<<cnt[bkt], 256, jsmem, st>>>(db, od + start, ws);
+        } else if (bkt == 1) {
+          k_jacobi<512><<<cnt[bkt], 512, jsmem, st>>>(db, od + start, ws);
+        } else {
+          HH_CUDA(cudaFuncSetAttribute(k_jacobi<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(double) * JAC_SMEM_K * JAC_SMEM_K)));
+          k_jacobi<1024><<<cnt[bkt], 1024, jsmem, st>>>(db, od + start, ws);
+        }
+        HH_LAUNCHED();
+        start += cnt[bkt];
+      }
+    }
     mark(5);
     if (!write) {  // pass 2 knows the rank: no residual / decision needed
       k_resid<<<(unsigned)tR.size(), THREADS, 0, st>>>(dR, db, ws, pts, H->N, H->d, K, partb.as<double>());

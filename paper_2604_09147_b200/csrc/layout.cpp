@@ -362,7 +362,18 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
   // leaves stay in Morton order: CTAs taking consecutive leaves from the counter work on
   // siblings at the same time, so the z slices of their shared ancestors' groups are read
   // from L2 (ncu: LPT order cost ~4% extra DRAM reads in phase 2 at 3D N=2^20)
+#ifdef HH_P2_LPT
+  {
+    std::vector<size_t> ord(leaves.size());
+    for (size_t k = 0; k < ord.size(); ++k) ord[k] = k;
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t c) { return lbytes[a] > lbytes[c]; });
+    std::vector<P2Leaf> l2(leaves.size());
+    for (size_t k = 0; k < ord.size(); ++k) l2[k] = leaves[ord[k]];
+    leaves.swap(l2);
+  }
+#else
   (void)lbytes;
+#endif
 }
 
 }  // namespace hh

@@ -20,7 +20,7 @@ import parity_lib as PL  # noqa: E402
 from paper_2604_09147_b200 import hh  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SMALL = ["2d_tiny", "2d_fig8_e4", "2d_fig8_e2", "3d_small_inv_r", "3d_small_exp"]
+SMALL = ["2d_tiny", "2d_fig8_e4", "2d_fig8_e2", "3d_small_inv_r", "3d_small_exp", "3d_sphere_small", "2d_circle_small"]
 
 
 @pytest.fixture(scope="module", params=SMALL)

@@ -32,6 +32,14 @@ def points_uniform(n: int, d: int, seed: int, lo: float = 0.0, hi: float = 1.0) 
     return np.ascontiguousarray(lo + (hi - lo) * rng.random((n, d)), dtype=np.float64)
 
 
+def points_sphere(n: int, d: int, seed: int) -> np.ndarray:
+    """N points on the surface of the unit hypersphere in R^d (the paper's P_circ set,
+    PAPER.md:1091): normalised standard-normal vectors (uniform on the sphere), float64."""
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((n, d))
+    return np.ascontiguousarray(g / np.linalg.norm(g, axis=1, keepdims=True), dtype=np.float64)
+
+
 def points_grid_centres(d: int, L: int) -> np.ndarray:
     """One point at the centre of every cell of a 2^L-per-axis grid (used by golden
     partition pins: with n_max=1 the depth rule yields exactly L and no empty cell)."""
@@ -82,18 +90,29 @@ SMALL_CONFIGS = {
                            eps=1e-6, pset=P_MIXED, nrhs=1, xdist="normal"),
     "3d_small_exp": dict(k=13, N=8000, d=3, kernel=K_EXP, scale=0.1, leaf=64, eta=1.0, s=2,
                          eps=1e-6, pset=P_MIXED, nrhs=4, xdist="normal"),
+    # NEXT-4: points on the unit sphere (App. D) — most
+    # leaf boxes empty, unbalanced occupancy (reading G20: empty clusters are skipped)
+    "3d_sphere_small": dict(k=14, N=8000, d=3, kernel=K_INV_R, scale=1.0, leaf=64, eta=1.0, s=3,
+                            eps=1e-6, pset=P_MIXED, nrhs=1, xdist="normal", points="sphere"),
+    "2d_circle_small": dict(k=15, N=6000, d=2, kernel=K_LOG, scale=1.0, leaf=32, eta=1.0, s=3,
+                            eps=1e-4, pset=P_MIXED, nrhs=1, xdist="uniform_pm1", points="sphere"),
 }
 
 
 # Iteration proxy for the 3D N=2^20 config (same kernel, eps, leaf occupancy ~32; 8x fewer
 # points so it builds in seconds).  Not a BASELINE config: used by scripts/profile_matvec.py.
 PROXY_CONFIGS = {
+    # NEXT-4 at scale: 3D unit sphere surface, N=2^18, 1/r, eps=1e-6 (bench with --config)
+    "3d_sphere": dict(k=21, N=262144, d=3, kernel=K_INV_R, scale=1.0, leaf=128, eta=1.0, s=4,
+                      eps=1e-6, pset=P_MIXED, nrhs=1, xdist="normal", points="sphere"),
     "3d_exp_proxy": dict(k=20, N=131072, d=3, kernel=K_EXP, scale=0.1, leaf=64, eta=1.0, s=3,
                          eps=1e-6, pset=P_MIXED, nrhs=1, xdist="normal"),
 }
 
 
 def make_points(cfg: dict) -> np.ndarray:
+    if cfg.get("points") == "sphere":
+        return points_sphere(cfg["N"], cfg["d"], 1000 + cfg["k"])
     return points_uniform(cfg["N"], cfg["d"], 1000 + cfg["k"], cfg.get("lo", 0.0), cfg.get("hi", 1.0))
 
 
