@@ -245,8 +245,8 @@ void compute_layout(hh_matrix *H) {
 // ----------------------------------------------------------------- matvec work plan
 // Phase 1: one item per W column tile, largest first (the kernels take items from a work
 // counter, so big tiles start early).  zmap[zbase + c] = z index of tile column c.
-// Phase 2: per leaf, dense segments then per tag the levels' U column groups; leaves in
-// Morton order.
+// Phase 2: per leaf, dense segments then per tag the levels' U column groups; leaves with
+// the most bytes first.
 void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &zmap, std::vector<P1Combine> &comb,
                 int64_t &npartial, std::vector<P2Seg> &segs, std::vector<P2Leaf> &leaves) {
   const size_t nb = H->level.size();
@@ -359,10 +359,10 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
     leaves.push_back(lf);
     lbytes.push_back(bytes);
   }
-  // leaves stay in Morton order: CTAs taking consecutive leaves from the counter work on
-  // siblings at the same time, so the z slices of their shared ancestors' groups are read
-  // from L2 (ncu: LPT order cost ~4% extra DRAM reads in phase 2 at 3D N=2^20)
-#ifdef HH_P2_LPT
+  // leaves with the most bytes first (LPT): measured ~4% faster in phase 2 than Morton order
+  // (profiles/r01_variants.txt), although Morton order re-reads fewer z slices from DRAM
+  // (ncu: LPT costs ~4% extra phase-2 DRAM reads at 3D N=2^20) — the tail balance wins
+#ifndef HH_P2_MORTON
   {
     std::vector<size_t> ord(leaves.size());
     for (size_t k = 0; k < ord.size(); ++k) ord[k] = k;

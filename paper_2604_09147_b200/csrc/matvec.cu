@@ -425,6 +425,7 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
   // --------------------------------------------------------------------- consumers
   constexpr int MB = mblock<NR>();
   const int tid = threadIdx.x;
+  int cur_ct = -1, slots = 1, Q = 1, cs = 0, q = 0;
   double acc[MB][NR];
   int32_t zi[MB];
   for (int n = 0;; ++n) {
@@ -434,10 +435,15 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
     const Meta m = *reinterpret_cast<const Meta *>(st + G::WBUF + G::XBUF);
     if (m.kind) break;
     const int ct = m.a;
-    const int slots = (ct + MB - 1) / MB;  // thread column slot cs owns columns cs + b * slots
-    int Q = 1;  // row groups: power of two <= 8 with Q * slots <= NCT (a column's lanes share a warp)
-    while (Q < 8 && 2 * Q * slots <= NCT) Q <<= 1;
-    const int cs = tid / Q, q = tid % Q;
+    if (ct != cur_ct) {  // thread layout of this tile width (recomputed only when it changes)
+      cur_ct = ct;
+      slots = (ct + MB - 1) / MB;  // thread column slot cs owns columns cs + b * slots
+      int lq = 0;                  // Q = 2^lq row groups, <= 8, Q * slots <= NCT (lanes of a column share a warp)
+      while (lq < 3 && (2 << lq) * slots <= NCT) ++lq;
+      Q = 1 << lq;
+      cs = tid >> lq;
+      q = tid & (Q - 1);
+    }
     const bool active = cs < slots;
     bool valid[MB];
 #pragma unroll
@@ -548,6 +554,7 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
   int kbase = 0;  // K-step parity offset: windows of a leaf continue the K-step numbering
+  int cur_nr = -1, MG = 1, KS = 1, mg = 0, ks = 0;
   for (int n = 0;; ++n) {
     const int s = n % G::STAGES;
     mbar_wait(&full[s], (n / G::STAGES) & 1);
@@ -555,15 +562,20 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
     const Meta m = *reinterpret_cast<const Meta *>(st + G::WBUF + G::XBUF);
     if (m.kind) break;
     const int nr = m.a;
-    const int MG = (nr + 31) / 32;
-    const int KS = max(1, NCW / MG);
-    const int mg = warp % MG, ks = warp / MG;
+    if (nr != cur_nr) {  // per-leaf warp layout (integer divisions only when the leaf size changes)
+      cur_nr = nr;
+      MG = (nr + 31) / 32;
+      KS = max(1, NCW / MG);
+      mg = warp % MG;
+      ks = warp / MG;
+    }
     const bool active = warp < MG * KS;
     const int ncols = m.r1 - m.r0;
     if (active) {
       const uint8_t *ust = st + m.wlead;
       const double *zst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
-      const int kfirst = ((ks - kbase) % KS + KS) % KS;
+      int kfirst = ks - kbase;
+      if (kfirst < 0) kfirst += KS;
       switch (m.b & 0xff) {
         case TAG_FP64: p2_mma_cols<TAG_FP64, NR>(ust, zst, ncols, nr, mg * 32, kfirst, KS, lane, c); break;
         case TAG_FP32: p2_mma_cols<TAG_FP32, NR>(ust, zst, ncols, nr, mg * 32, kfirst, KS, lane, c); break;
@@ -571,7 +583,12 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
         default: p2_mma_cols<TAG_BF16, NR>(ust, zst, ncols, nr, mg * 32, kfirst, KS, lane, c); break;
       }
     }
-    kbase = (kbase + (ncols + 3) / 4) % KS;
+    if (KS == 1) {
+      kbase = 0;
+    } else {
+      kbase += (ncols + 3) >> 2;
+      while (kbase >= KS) kbase -= KS;
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (m.flags & 1) {
@@ -679,6 +696,7 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
   // --------------------------------------------------------------------- consumers
   constexpr int MB = mblock<NR>();
   const int tid = threadIdx.x;
+  int cur_nr = -1, nr2 = 1, Gn = 1, rr = 0, g = 0;
   double acc[MB][NR];
 #pragma unroll
   for (int b = 0; b < MB; ++b)
@@ -691,9 +709,13 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
     const Meta m = *reinterpret_cast<const Meta *>(st + G::WBUF + G::XBUF);
     if (m.kind) break;
     const int nr = m.a;
-    const int nr2 = (nr + MB - 1) / MB;  // thread row slot rr owns rows rr + b * nr2
-    const int Gn = NCT / nr2;            // column groups (nr <= 256: leaf_size limit)
-    const int rr = tid % nr2, g = tid / nr2;
+    if (nr != cur_nr) {  // thread layout of this leaf size (divisions only when it changes)
+      cur_nr = nr;
+      nr2 = (nr + MB - 1) / MB;  // thread row slot rr owns rows rr + b * nr2
+      Gn = NCT / nr2;            // column groups (nr <= 256: leaf_size limit)
+      rr = tid % nr2;
+      g = tid / nr2;
+    }
     bool valid[MB];
 #pragma unroll
     for (int b = 0; b < MB; ++b) valid[b] = g < Gn && rr + b * nr2 < nr;

@@ -95,6 +95,12 @@ __global__ void k_gather_pts(const double *__restrict__ P, int64_t N, int d, con
   }
 }
 
+// flag = 1 if some run of equal sorted keys is longer than n_max (key[i] == key[i + n_max])
+__global__ void k_long_run(const uint64_t *__restrict__ key, int64_t N, int nmax, int *flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + nmax < N; i += (int64_t)gridDim.x * blockDim.x)
+    if (key[i] == key[i + nmax]) *flag = 1;
+}
+
 inline int grid_for(int64_t n, int threads = 256) {
   int64_t g = (n + threads - 1) / threads;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
@@ -141,7 +147,30 @@ void build_tree(hh_matrix *H, const double *P, cudaStream_t st, DBuf &pts_tree) 
   int L = 0;
   for (;; ++L) {
     HH_REQUIRE((int64_t)d * L <= 62, HH_EDEPTH, "d*L exceeds 62 bits before every leaf holds <= leaf_size points");
-    HH_REQUIRE(d * L <= MAX_CELL_BITS, HH_EUNSUPPORTED, "more than 2^26 leaf cells needed");
+    if (d * L > MAX_CELL_BITS) {
+      // beyond this build's cell limit: report HH_EDEPTH when even the deepest 62-bit keys
+      // leave more than leaf_size points in one cell (e.g. duplicated points), else unsupported
+      const int Lmax = 62 / d;
+      DBuf k1, k2, ix, flag, tb;
+      k1.alloc(sizeof(uint64_t) * N);
+      k2.alloc(sizeof(uint64_t) * N);
+      ix.alloc(sizeof(int32_t) * N);
+      flag.alloc(sizeof(int));
+      HH_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+      k_keys<<<grid_for(N), 256, 0, st>>>(P, N, d, C, Lmax, k1.as<uint64_t>(), ix.as<int32_t>());
+      HH_LAUNCHED();
+      size_t tmp = 0;
+      cub::DeviceRadixSort::SortKeys(nullptr, tmp, k1.as<uint64_t>(), k2.as<uint64_t>(), (int)N, 0, d * Lmax, st);
+      tb.alloc(tmp);
+      HH_CUDA(cub::DeviceRadixSort::SortKeys(tb.p, tmp, k1.as<uint64_t>(), k2.as<uint64_t>(), (int)N, 0, d * Lmax, st));
+      k_long_run<<<grid_for(N), 256, 0, st>>>(k2.as<uint64_t>(), N, H->leaf_size, flag.as<int>());
+      HH_LAUNCHED();
+      int hf = 0;
+      HH_CUDA(cudaMemcpyAsync(&hf, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      HH_CUDA(cudaStreamSynchronize(st));
+      HH_REQUIRE(!hf, HH_EDEPTH, "d*L exceeds 62 bits before every leaf holds <= leaf_size points (duplicated points)");
+      HH_REQUIRE(false, HH_EUNSUPPORTED, "more than 2^26 leaf cells needed");
+    }
     const int64_t ncell = 1ll << (d * L);
     hist.alloc(sizeof(int) * ncell);
     HH_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(int) * ncell, st));
