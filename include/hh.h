@@ -136,6 +136,24 @@ hh_status hh_matvec_host(hh_handle H, const double *x_host, double *y_host, int3
 hh_status hh_matvec_profile(hh_handle H, int32_t enable);
 hh_status hh_matvec_timing(hh_handle H, double *ms, int64_t *count);
 
+/*
+ * hh_switch_level_search — Alg. 5 (alg:algo_optimal_level): the switching
+ * level ell* maximising S_1(ell) - S_2(ell) (Eqs. S1/S2), i.e. the H_h with the
+ * least storage relative to the pure standard H (H_s).  Bottom-up as in the paper: ell = L
+ * (Alg. 1's ell = L branch is H_s, so S_1(L) = S_2(L)), then ell - 1 while the gain
+ * S_s - S_h(ell - 1) grows.  Storage comes from ledger-only builds (ranks, tags and bytes,
+ * nothing stored), counted in each block's storage bits — the mixed-precision variant the
+ * paper leaves open; with precision_set = HH_P_FP64 it is the uniform one.
+ *   points, N, d, kernel, eps, eta, leaf_size, precision_set, cuda_stream: as hh_build.
+ *   out_level  receives ell* in [0, L]; ell* = L means H_s (build it with HH_SWITCH_NONE).
+ *   bytes      optional host int64 array of bytes_len >= L + 2 entries: bytes[l] = S_h(l) for the
+ *              levels visited (-1 for the others), bytes[L + 1] = S_s.  NULL to skip;
+ *              HH_EINVAL if bytes_len is too small (L is reported in out_L when non-NULL).
+ */
+hh_status hh_switch_level_search(const double *points, int64_t N, int32_t d, hh_kernel kernel, double eps,
+                                 double eta, int32_t leaf_size, uint32_t precision_set, void *cuda_stream,
+                                 int32_t *out_level, int32_t *out_L, int64_t *bytes, int32_t bytes_len);
+
 /* Summary of a built handle (always available, host memory, filled by hh_info). */
 typedef struct {
   int32_t d, L, switch_level, kernel_kind;

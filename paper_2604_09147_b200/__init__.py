@@ -6,7 +6,8 @@ binding is imported lazily so that ``build`` runs before the library exists; tou
 binding name without a built library raises (there is no CPU fallback).
 """
 _BINDING = ("EXPORTED", "Handle", "HHError", "hh_build", "hh_export", "hh_free", "hh_info", "hh_matvec",
-            "hh_matvec_host", "hh_matvec_profile", "hh_matvec_timing", "kernel_launches", "selftest_round")
+            "hh_matvec_host", "hh_matvec_profile", "hh_matvec_timing", "kernel_launches", "selftest_round",
+            "hh_switch_level_search")
 
 
 def __getattr__(name):

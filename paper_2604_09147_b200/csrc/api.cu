@@ -428,6 +428,48 @@ hh_status hh_export(hh_handle H, hh_export_t *out) {
   }
 }
 
+hh_status hh_switch_level_search(const double *points, int64_t N, int32_t d, hh_kernel kernel, double eps,
+                                 double eta, int32_t leaf_size, uint32_t precision_set, void *cuda_stream,
+                                 int32_t *out_level, int32_t *out_L, int64_t *bytes, int32_t bytes_len) {
+  g_err.clear();
+  if (!out_level) return fail(HH_EINVAL, "NULL pointer");
+  const uint32_t pset = (precision_set & 0xFu) | HH_LEDGER_ONLY;
+  auto ledger_bytes = [&](int32_t s, int64_t &out, int32_t *L) -> hh_status {
+    hh_handle h = nullptr;
+    const hh_status st = hh_build(points, N, d, kernel, eps, eta, leaf_size, s, pset, cuda_stream, &h);
+    if (st != HH_OK) return st;
+    out = h->info.stored_bytes;
+    if (L) *L = h->L;
+    hh_free(h);
+    return HH_OK;
+  };
+  int64_t Ss = 0;
+  int32_t L = 0;
+  hh_status st = ledger_bytes(HH_SWITCH_NONE, Ss, &L);  // S_s: pure H_s (the paper's ell = L)
+  if (st != HH_OK) return st;
+  if (out_L) *out_L = L;
+  if (bytes && bytes_len < L + 2) return fail(HH_EINVAL, "bytes_len must be >= L + 2");
+  if (bytes) {
+    for (int i = 0; i < L + 2; ++i) bytes[i] = -1;
+    bytes[L] = Ss;
+    bytes[L + 1] = Ss;
+  }
+  int32_t ell = L;
+  int64_t gain = 0;  // S_1(L) - S_2(L) = 0
+  while (ell > 0) {
+    int64_t Sh = 0;
+    st = ledger_bytes(ell - 1, Sh, nullptr);
+    if (st != HH_OK) return st;
+    if (bytes) bytes[ell - 1] = Sh;
+    const int64_t gnew = Ss - Sh;  // S_1(ell-1) - S_2(ell-1): the common terms cancel
+    if (gnew <= gain) break;
+    gain = gnew;
+    --ell;
+  }
+  *out_level = ell;
+  return HH_OK;
+}
+
 hh_status hh_free(hh_handle H) {
   delete H;
   return HH_OK;

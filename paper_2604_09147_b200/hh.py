@@ -85,18 +85,22 @@ def _load():
     lib.hh_free.argtypes = [C.c_void_p]
     lib.hh_last_error.restype = C.c_char_p
     lib.hh_kernel_launches.restype = C.c_int64
+    lib.hh_switch_level_search.argtypes = [C.c_void_p, C.c_int64, C.c_int32, hh_kernel, C.c_double, C.c_double,
+                                           C.c_int32, C.c_uint32, C.c_void_p, C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_int32), C.c_void_p, C.c_int32]
     lib.hh_selftest_round.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]
     lib.hh_matvec_profile.argtypes = [C.c_void_p, C.c_int32]
     lib.hh_matvec_timing.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     for f in ("hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_selftest_round",
-              "hh_matvec_profile", "hh_matvec_timing"):
+              "hh_matvec_profile", "hh_matvec_timing", "hh_switch_level_search"):
         getattr(lib, f).restype = C.c_int
     return lib
 
 
 lib = _load()
 EXPORTED = ["hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_last_error",
-            "hh_kernel_launches", "hh_selftest_round", "hh_matvec_profile", "hh_matvec_timing"]
+            "hh_kernel_launches", "hh_selftest_round", "hh_matvec_profile", "hh_matvec_timing",
+            "hh_switch_level_search"]
 
 
 def _check(st):
@@ -210,6 +214,20 @@ def hh_matvec_timing(H: Handle) -> tuple[list, int]:
     n = C.c_int64()
     _check(lib.hh_matvec_timing(H.ptr, ms, C.byref(n)))
     return list(ms), int(n.value)
+
+
+def hh_switch_level_search(points, kernel: int, scale: float, eps: float, eta: float, leaf_size: int,
+                           precision_set: int, stream=None) -> tuple[int, list]:
+    """Alg. 5 (switching-level search) on ledger-only builds.  points: torch CUDA float64 (N, d).
+    Returns (ell*, bytes) with bytes[l] = S_h(l) (-1 if not visited) and bytes[L+1] = S_s."""
+    assert points.is_cuda and points.dtype.is_floating_point and points.is_contiguous()
+    n, d = points.shape
+    lvl, L = C.c_int32(), C.c_int32()
+    buf = np.full(70, -1, np.int64)
+    _check(lib.hh_switch_level_search(C.c_void_p(points.data_ptr()), n, d, hh_kernel(kernel, scale), eps, eta,
+                                      leaf_size, precision_set, _stream_ptr(stream), C.byref(lvl), C.byref(L),
+                                      buf.ctypes.data, buf.size))
+    return int(lvl.value), buf[:L.value + 2].tolist()
 
 
 def hh_free(H: Handle):

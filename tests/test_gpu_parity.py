@@ -266,3 +266,16 @@ print("row-split ok")
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "row-split ok" in out.stdout
+
+
+def test_switch_level_search_matches_oracle():
+    """NEXT-2: Alg. 5 on ledger-only builds equals the oracle's walk on its
+    own builds — the same ell* and the same storage at every visited level (bits-aware)."""
+    from oracle import switch_level as SL
+    P = W.points_uniform(1500, 2, 31)
+    args = (W.K_LOG, 1.0, 1e-6, 1.0, 24, W.P_MIXED)
+    ell_o, L, by_o = SL.alg_lstar(P, *args)
+    Pd = torch.from_numpy(P).cuda()
+    ell_g, by_g = hh.hh_switch_level_search(Pd, *args)
+    assert len(by_g) == L + 2
+    assert ell_g == ell_o and by_g == by_o, (ell_g, ell_o, by_g, by_o)
