@@ -231,7 +231,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2604_09147_b200 import hh
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    cfg = dict(W.CONFIGS[args.config])
+    cfg = dict(W.CONFIGS.get(args.config) or W.PROXY_CONFIGS[args.config])
     if args.switch is not None:
         cfg["s"] = args.switch
     if args.pset is not None:
@@ -389,7 +389,7 @@ def run_ours(args, rank, world, local_rank):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    cfg = W.CONFIGS[args.config]
+    cfg = W.CONFIGS.get(args.config) or W.PROXY_CONFIGS[args.config]
     # size of the workload's stored bytes is a property of the method; the reference arm
     # reports the oracle's GB/s over its own bounded sample and the equivalent matvecs/s
     # against the GPU build's stored bytes recorded in profiles/ (if present)
@@ -417,7 +417,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="3d_large", choices=list(W.CONFIGS))
+    ap.add_argument("--config", default="3d_large", choices=list(W.CONFIGS) + list(W.PROXY_CONFIGS))
     ap.add_argument("--nrhs", type=int, default=1)
     ap.add_argument("--switch", type=int, default=None)
     ap.add_argument("--pset", type=int, default=None)

@@ -185,3 +185,27 @@ def stored_bytes(H: OracleH) -> dict:
             lr += nbytes
             by_tag[int(H.tag[b])] += nbytes
     return dict(lowrank=lr, dense=dn, total=lr + dn, by_tag=by_tag)
+
+
+def ranks_only(P, kernel, scale, eps, eta, leaf, s, L_force=None):
+    """Partition + truncated-SVD ranks only (singular values, no vectors) — for storage
+    studies (Table 3) where factors are not needed.  Returns
+    (tree, partition, rank[], m[], n[]) with rank = -1 for blocks kept dense."""
+    from scipy.linalg import svdvals
+    from .compress import truncation_rank
+    tr = build_tree(P, leaf)
+    part = build_partition(tr, eta, s)
+    nb = len(part)
+    rank = np.full(nb, -1, np.int64)
+    m = np.zeros(nb, np.int64)
+    n = np.zeros(nb, np.int64)
+    for b in range(nb):
+        l = int(part.level[b])
+        i0, i1 = tr.cluster(l, int(part.tgt[b]))
+        j0, j1 = tr.cluster(l, int(part.src[b]))
+        m[b], n[b] = i1 - i0, j1 - j0
+        if part.kind[b] in (DIAG, LNBR):
+            continue
+        A, _ = kernel_block(P, tr.perm[i0:i1], tr.perm[j0:j1], kernel, scale)
+        rank[b] = truncation_rank(svdvals(A), eps)[0] if A.size else 0
+    return tr, part, rank, m, n

@@ -109,6 +109,10 @@ struct hh_matrix {
   int64_t n_p1_tiles = 0, n_p2_leaves = 0, n_p1_comb = 0, n_partial = 0;
   hh::DBuf v;        // [(N + ztotal) * 16] doubles (+ slack for 16-B aligned superset copies)
   hh::DBuf ctr;      // work counters of the persistent matvec kernels (zeroed by the gather)
+  struct LaunchCfg {  // per RHS-chunk width (1, 2, 4, 8, 16): set once, reused by every hh_matvec
+    bool ready = false;
+    int nsm = 0, grid1 = 0, grid2 = 0;
+  } lcfg[5];
   hh::DBuf hx, hy;   // staging for hh_matvec_host
   // optional per-phase timing of the matvec (hh_matvec_profile)
   bool prof = false;

@@ -5,8 +5,9 @@
 //   a8  phase 1:  z_b = W_b^T x_J for every low-rank block.  W is stored as per-source
 //                 panels: for a source cluster J all blocks b with src J form
 //                 one |J| x P_J matrix, cut into column tiles of <= 248 columns stored
-//                 row-major.  One work item = one tile; thread c of the CTA owns tile column
-//                 c and accumulates it over all |J| rows, so z needs no second pass.
+//                 row-major.  One work item = one tile (tiles taller than 4096 rows: one
+//                 row piece, summed by a fixed-order combine pass); thread c of the CTA owns
+//                 tile column c and accumulates it over the rows.
 //   a9  phase 2:  per leaf R (one owner, fixed order, no atomics):
 //                 y_R = sum_dense D_RJ x_J + sum_{tags, levels} U_{R,l,g} z_{l,g}
 //   a10 scatter:  fused into the phase-2 epilogue, y[perm[t]] = y~[t]
@@ -15,9 +16,10 @@
 //
 // Both phases are persistent kernels (grid = resident CTAs) that take work items from a
 // counter.  One producer thread streams each item through a ring of shared-memory stages
-// with cp.async.bulk (TMA bulk copies completing on an mbarrier): the factor window (<= 16
+// with cp.async.bulk (TMA bulk copies completing on an mbarrier): the factor window (<= 32
 // KiB) AND the matching vector slice (x~ rows for phase 1, z entries for phase 2) plus a
 // small descriptor, so the 8 consumer warps never touch global memory in their inner loops.
+// Consumers: fp64 FMA (DFMA) at NR = 1, 2, 4; FP64 tensor cores (DMMA) at NR = 8, 16.
 #include <algorithm>
 #include <vector>
 
@@ -38,7 +40,7 @@ constexpr int THREADS = NCT + 32;      // + one producer warp
 #endif
 // Stage geometry.  Measured on B200 (profiles/r01_variants.txt): fewer, larger stages with
 // more CTAs per SM win — 2 stages of 32 KiB factor data at 3 CTAs/SM for NR <= 2; the
-// FP64-bound multi-RHS kernels (NR >= 4) keep 3 stages at 1 CTA/SM.
+// FP64-bound multi-RHS kernels size the vector slice per phase (see Geo).
 #ifndef HH_MV_WDATA
 #define HH_MV_WDATA 32768
 #endif
@@ -376,10 +378,15 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
     if (lane != 0) return;
     const uint64_t pol_w = evict_first_policy(), pol_x = evict_last_policy();
     int n = 0;
+    // the next item index and its descriptor are requested one item ahead, so their latency
+    // overlaps the current item's stage issue (small tiles are ~1 us of streaming each)
     int item = atomicAdd(a.ctr, 1);
+    P1Tile Tn{};
+    if (item < a.ntiles) Tn = a.tiles[item];
     while (item < a.ntiles) {
-      const P1Tile T = a.tiles[item];
+      const P1Tile T = Tn;
       const int nxt = atomicAdd(a.ctr, 1);
+      if (nxt < a.ntiles) Tn = a.tiles[nxt];
       const int w = tag_bytes(T.tag);
       const int rowb = T.ct * w;
       const int rs = max(1, min(G::XELEMS / NR, G::WDATA / rowb));
@@ -645,12 +652,18 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
     if (lane != 0) return;
     const uint64_t pol_w = evict_first_policy(), pol_x = evict_last_policy();
     int n = 0;
+    // next leaf index / descriptor and the next segment descriptor are fetched one ahead
     int li = atomicAdd(a.ctr + 1, 1);
+    P2Leaf Ln{};
+    if (li < a.nleaves) Ln = a.leaves[li];
     while (li < a.nleaves) {
-      const P2Leaf Lf = a.leaves[li];
+      const P2Leaf Lf = Ln;
       const int nxt = atomicAdd(a.ctr + 1, 1);
+      if (nxt < a.nleaves) Ln = a.leaves[nxt];
+      P2Seg Sn = a.segs[Lf.s0];
       for (int64_t si = Lf.s0; si < Lf.s1; ++si) {
-        const P2Seg S = a.segs[si];
+        const P2Seg S = Sn;
+        if (si + 1 < Lf.s1) Sn = a.segs[si + 1];
         const int w = tag_bytes(S.tag);
         const int colb = Lf.nr * w;
         const int cs = max(1, min(G::XELEMS / NR, G::WDATA / colb));
@@ -785,9 +798,22 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   using namespace mv;
   using G1 = Geo<NR, 1>;
   using G2 = Geo<NR, 2>;
-  int dev = 0, nsm = 148;
-  HH_CUDA(cudaGetDevice(&dev));
-  HH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  // launch geometry (device attributes, smem opt-in, occupancy) once per handle and width
+  hh_matrix::LaunchCfg &L = H->lcfg[NR == 1 ? 0 : NR == 2 ? 1 : NR == 4 ? 2 : NR == 8 ? 3 : 4];
+  if (!L.ready) {
+    int dev = 0;
+    HH_CUDA(cudaGetDevice(&dev));
+    HH_CUDA(cudaDeviceGetAttribute(&L.nsm, cudaDevAttrMultiProcessorCount, dev));
+    HH_CUDA(cudaFuncSetAttribute(k_phase1<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem(false)));
+    HH_CUDA(cudaFuncSetAttribute(k_phase2<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::smem(true)));
+    int p1 = 0, p2 = 0;
+    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_phase1<NR>, THREADS, G1::smem(false)));
+    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_phase2<NR>, THREADS, G2::smem(true)));
+    L.grid1 = (int)std::min<int64_t>(H->n_p1_tiles, (int64_t)L.nsm * std::max(1, p1));
+    L.grid2 = (int)std::min<int64_t>(H->n_p2_leaves, (int64_t)L.nsm * std::max(1, p2));
+    L.ready = true;
+  }
+  const int nsm = L.nsm;
   double *v = H->v.as<double>();
   int *ctr = H->ctr.as<int>();
   cudaEvent_t ev[4];
@@ -813,16 +839,7 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     a.v = v;
     a.N = H->N;
     a.ctr = ctr;
-    const size_t sm = G1::smem(false);
-    static bool attr1[17] = {};
-    if (!attr1[NR]) {
-      HH_CUDA(cudaFuncSetAttribute(k_phase1<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      attr1[NR] = true;
-    }
-    int per_sm = 0;
-    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_phase1<NR>, THREADS, sm));
-    const int64_t grid = std::min<int64_t>(H->n_p1_tiles, (int64_t)nsm * std::max(1, per_sm));
-    k_phase1<NR><<<(unsigned)grid, THREADS, sm, st>>>(a);
+    k_phase1<NR><<<(unsigned)L.grid1, THREADS, G1::smem(false), st>>>(a);
     HH_LAUNCHED();
     if (H->n_p1_comb > 0) {
       k_p1_combine<NR><<<(unsigned)std::min<int64_t>(H->n_p1_comb, (int64_t)nsm * 8), 256, 0, st>>>(
@@ -843,17 +860,8 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   b.y = y + (int64_t)col0 * H->N;
   b.ldy = H->N;
   b.ctr = ctr;
-  const size_t sm2 = G2::smem(true);
-  static bool attr2[17] = {};
-  if (!attr2[NR]) {
-    HH_CUDA(cudaFuncSetAttribute(k_phase2<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-    attr2[NR] = true;
-  }
-  int per_sm2 = 0;
-  HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_phase2<NR>, THREADS, sm2));
-  const int64_t grid2 = std::min<int64_t>(H->n_p2_leaves, (int64_t)nsm * std::max(1, per_sm2));
-  if (grid2 > 0) {
-    k_phase2<NR><<<(unsigned)grid2, THREADS, sm2, st>>>(b);
+  if (L.grid2 > 0) {
+    k_phase2<NR><<<(unsigned)L.grid2, THREADS, G2::smem(true), st>>>(b);
     HH_LAUNCHED();
   }
   mark(3);

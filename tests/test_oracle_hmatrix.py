@@ -295,3 +295,25 @@ def test_alg_lstar_follows_the_bottom_up_rule():
         if by[l] >= 0:
             assert by[l] == full[l]
     assert (full + [Ss])[ell] <= Ss
+
+
+@pytest.mark.slow
+def test_table3_s1_over_s2_3d_inv_r():
+    """Table 3: S_1(ell)/S_2(ell) at ell = L-1 for 3D 1/r, N=64000 uniform in
+    [-1,1]^3, L=3 (n_max=125 in the paper's balanced-tree formula), eta=sqrt(3), eps=1e-6:
+    printed 1.60.  Storage in words (uniform precision); units of the printed S_1, S_2 are
+    unstated, so only the ratio is pinned, with a band for the unknown point seed
+    (1.60 +- 0.15).  Slow: ~10^5 SVDs (not in the default CPU suite)."""
+    from oracle.partition import FAR, LNBR, NBR, SIB
+    P = W.points_uniform(64000, 3, 64000, -1.0, 1.0)
+    eta, eps = np.sqrt(3.0), 1e-6
+    leaf = 260   # the depth rule then gives L = 3 (max leaf ~ 170 > 125, the paper's balanced count)
+    trs, ps, rs, ms, ns = HM.ranks_only(P, W.K_INV_R, 1.0, eps, eta, leaf, PT.SWITCH_NONE)
+    assert trs.L == 3
+    ell = trs.L - 1
+    S1 = int(np.sum((rs * (ms + ns))[(ps.level > ell) & (ps.kind == FAR)])) + int(np.sum((ms * ns)[ps.kind == LNBR]))
+    trh, ph, rh, mh, nh = HM.ranks_only(P, W.K_INV_R, 1.0, eps, eta, leaf, ell)
+    S2 = int(np.sum((rh * (mh + nh))[((ph.level == ell) & (ph.kind == NBR)) | ((ph.level > ell) & (ph.kind == SIB))]))
+    ratio = S1 / S2
+    print("Table 3 L=3 eps=1e-6: S1/S2 =", ratio)
+    assert 1.45 <= ratio <= 1.75, ratio
