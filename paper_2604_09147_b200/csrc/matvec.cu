@@ -283,15 +283,15 @@ __device__ __forceinline__ void block_acc(const typename Elem<TAG>::T *e, const 
 // Phase-1 DMMA consumer (NR = 8, 16): warp w owns tile columns [32w, 32w + 32) as four
 // 8-column M-tiles; each 4-row K-step does 4 x NR/8 DMMAs.  Accumulators persist over the
 // tile's row windows; z is written at the last one.
-template <int TAG, int NR>
-__device__ __forceinline__ void p1_mma_rows(const uint8_t *wst, const double *xst, int nrows, int ct, int col0,
-                                            int lane, double (&c)[4][NR / 8][2]) {
+template <int TAG, int NR, int MT>
+__device__ __forceinline__ void p1_mma_rows_t(const uint8_t *wst, const double *xst, int nrows, int ct, int col0,
+                                              int lane, double (&c)[4][NR / 8][2]) {
   using T = typename Elem<TAG>::T;
   const T *W = reinterpret_cast<const T *>(wst);
   const int kq = lane & 3, mq = lane >> 2;
-  bool cv[4];
+  bool cv[MT];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) cv[mt] = col0 + mt * 8 + mq < ct;
+  for (int mt = 0; mt < MT; ++mt) cv[mt] = col0 + mt * 8 + mq < ct;
 #pragma unroll 2
   for (int k0 = 0; k0 < nrows; k0 += 4) {
     const int row = k0 + kq;
@@ -300,11 +300,24 @@ __device__ __forceinline__ void p1_mma_rows(const uint8_t *wst, const double *xs
 #pragma unroll
     for (int nt = 0; nt < NR / 8; ++nt) b[nt] = rv ? xst[row * NR + nt * 8 + mq] : 0.0;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
+    for (int mt = 0; mt < MT; ++mt) {
       const double av = (rv && cv[mt]) ? up<TAG>(W[row * ct + col0 + mt * 8 + mq]) : 0.0;
 #pragma unroll
       for (int nt = 0; nt < NR / 8; ++nt) dmma(c[mt][nt], av, b[nt]);
     }
+  }
+}
+
+// only the M-tiles that hold columns of the tile are multiplied (MT = 1..4, warp-uniform)
+template <int TAG, int NR>
+__device__ __forceinline__ void p1_mma_rows(const uint8_t *wst, const double *xst, int nrows, int ct, int col0,
+                                            int lane, double (&c)[4][NR / 8][2]) {
+  const int mtiles = min(4, (ct - col0 + 7) >> 3);
+  switch (mtiles) {
+    case 4: p1_mma_rows_t<TAG, NR, 4>(wst, xst, nrows, ct, col0, lane, c); break;
+    case 3: p1_mma_rows_t<TAG, NR, 3>(wst, xst, nrows, ct, col0, lane, c); break;
+    case 2: p1_mma_rows_t<TAG, NR, 2>(wst, xst, nrows, ct, col0, lane, c); break;
+    default: p1_mma_rows_t<TAG, NR, 1>(wst, xst, nrows, ct, col0, lane, c); break;
   }
 }
 
@@ -526,15 +539,15 @@ struct P2Args {
 // four (MG groups); warp w takes group w % MG and the K-steps (4 columns) k = w / MG (mod
 // KS), KS = NCW / MG.  At the leaf's last window the KS partial tiles of each group are
 // summed in a fixed order through shared memory and scattered to y (a10).
-template <int TAG, int NR>
-__device__ __forceinline__ void p2_mma_cols(const uint8_t *ust, const double *zst, int ncols, int nr, int row0,
-                                            int kfirst, int KS, int lane, double (&c)[4][NR / 8][2]) {
+template <int TAG, int NR, int MT>
+__device__ __forceinline__ void p2_mma_cols_t(const uint8_t *ust, const double *zst, int ncols, int nr, int row0,
+                                              int kfirst, int KS, int lane, double (&c)[4][NR / 8][2]) {
   using T = typename Elem<TAG>::T;
   const T *U = reinterpret_cast<const T *>(ust);
   const int kq = lane & 3, mq = lane >> 2;
-  bool rv[4];
+  bool rv[MT];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) rv[mt] = row0 + mt * 8 + mq < nr;
+  for (int mt = 0; mt < MT; ++mt) rv[mt] = row0 + mt * 8 + mq < nr;
 #pragma unroll 2
   for (int k0 = 4 * kfirst; k0 < ncols; k0 += 4 * KS) {
     const int col = k0 + kq;
@@ -543,11 +556,23 @@ __device__ __forceinline__ void p2_mma_cols(const uint8_t *ust, const double *zs
 #pragma unroll
     for (int nt = 0; nt < NR / 8; ++nt) b[nt] = cvl ? zst[col * NR + nt * 8 + mq] : 0.0;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
+    for (int mt = 0; mt < MT; ++mt) {
       const double av = (cvl && rv[mt]) ? up<TAG>(U[col * nr + row0 + mt * 8 + mq]) : 0.0;
 #pragma unroll
       for (int nt = 0; nt < NR / 8; ++nt) dmma(c[mt][nt], av, b[nt]);
     }
+  }
+}
+
+// only this group's M-tiles are multiplied (tcount = 1..4, warp-uniform)
+template <int TAG, int NR>
+__device__ __forceinline__ void p2_mma_cols(const uint8_t *ust, const double *zst, int ncols, int nr, int row0,
+                                            int tcount, int kfirst, int KS, int lane, double (&c)[4][NR / 8][2]) {
+  switch (tcount) {
+    case 4: p2_mma_cols_t<TAG, NR, 4>(ust, zst, ncols, nr, row0, kfirst, KS, lane, c); break;
+    case 3: p2_mma_cols_t<TAG, NR, 3>(ust, zst, ncols, nr, row0, kfirst, KS, lane, c); break;
+    case 2: p2_mma_cols_t<TAG, NR, 2>(ust, zst, ncols, nr, row0, kfirst, KS, lane, c); break;
+    default: p2_mma_cols_t<TAG, NR, 1>(ust, zst, ncols, nr, row0, kfirst, KS, lane, c); break;
   }
 }
 
@@ -561,7 +586,7 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
   int kbase = 0;  // K-step parity offset: windows of a leaf continue the K-step numbering
-  int cur_nr = -1, MG = 1, KS = 1, mg = 0, ks = 0;
+  int cur_nr = -1, MG = 1, KS = 1, mg = 0, ks = 0, tbeg = 0, tcnt = 0;
   for (int n = 0;; ++n) {
     const int s = n % G::STAGES;
     mbar_wait(&full[s], (n / G::STAGES) & 1);
@@ -571,10 +596,13 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
     const int nr = m.a;
     if (nr != cur_nr) {  // per-leaf warp layout (integer divisions only when the leaf size changes)
       cur_nr = nr;
-      MG = (nr + 31) / 32;
+      const int T = (nr + 7) >> 3;  // 8-row M-tiles of the leaf, dealt to MG groups of <= 4
+      MG = (T + 3) >> 2;
       KS = max(1, NCW / MG);
       mg = warp % MG;
       ks = warp / MG;
+      tbeg = mg * T / MG;           // balanced: group sizes differ by at most one tile
+      tcnt = (mg + 1) * T / MG - tbeg;
     }
     const bool active = warp < MG * KS;
     const int ncols = m.r1 - m.r0;
@@ -584,10 +612,10 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
       int kfirst = ks - kbase;
       if (kfirst < 0) kfirst += KS;
       switch (m.b & 0xff) {
-        case TAG_FP64: p2_mma_cols<TAG_FP64, NR>(ust, zst, ncols, nr, mg * 32, kfirst, KS, lane, c); break;
-        case TAG_FP32: p2_mma_cols<TAG_FP32, NR>(ust, zst, ncols, nr, mg * 32, kfirst, KS, lane, c); break;
-        case TAG_FP16: p2_mma_cols<TAG_FP16, NR>(ust, zst, ncols, nr, mg * 32, kfirst, KS, lane, c); break;
-        default: p2_mma_cols<TAG_BF16, NR>(ust, zst, ncols, nr, mg * 32, kfirst, KS, lane, c); break;
+        case TAG_FP64: p2_mma_cols<TAG_FP64, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
+        case TAG_FP32: p2_mma_cols<TAG_FP32, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
+        case TAG_FP16: p2_mma_cols<TAG_FP16, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
+        default: p2_mma_cols<TAG_BF16, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
       }
     }
     if (KS == 1) {
@@ -611,9 +639,12 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
       consumer_sync();
       // every warp finalises some of the MG x 4 x NT output fragments: fixed-order sum over
       // the KS k-slices, then the scatter y[perm[t]] (a10)
+      const int T = (nr + 7) >> 3;
       for (int f = warp; f < MG * 4 * NT; f += NCW) {
         const int g = f / (4 * NT), mt = (f / NT) % 4, nt = f % NT;
-        const int r = g * 32 + mt * 8 + (lane >> 2);
+        const int tb = g * T / MG, tc = (g + 1) * T / MG - tb;  // group g's tiles (as in the layout)
+        if (mt >= tc) continue;
+        const int r = (tb + mt) * 8 + (lane >> 2);
         if (r >= nr) continue;
         double s0 = 0.0, s1 = 0.0;
         for (int k = 0; k < KS; ++k) {

@@ -35,7 +35,7 @@ def _words(H):
 
 def test_table3_ratios():
     P = torch.from_numpy(W.points_uniform(64000, 3, 64000, -1.0, 1.0)).cuda()
-    eta, leaf = float(np.sqrt(3.0)), 260
+    eta, leaf = float(np.sqrt(3.0)), 250   # the depth rule gives L = 3 (max leaf ~170; the paper: 125 balanced)
     ratios = {}
     for eps in PAPER:
         Hs = hh.hh_build(P, W.K_INV_R, 1.0, eps, eta, leaf, W.SWITCH_NONE, W.P_FP64 | hh.LEDGER_ONLY)

@@ -307,7 +307,7 @@ def test_table3_s1_over_s2_3d_inv_r():
     from oracle.partition import FAR, LNBR, NBR, SIB
     P = W.points_uniform(64000, 3, 64000, -1.0, 1.0)
     eta, eps = np.sqrt(3.0), 1e-6
-    leaf = 260   # the depth rule then gives L = 3 (max leaf ~ 170 > 125, the paper's balanced count)
+    leaf = 250   # the depth rule then gives L = 3
     trs, ps, rs, ms, ns = HM.ranks_only(P, W.K_INV_R, 1.0, eps, eta, leaf, PT.SWITCH_NONE)
     assert trs.L == 3
     ell = trs.L - 1
