@@ -187,18 +187,37 @@ def stored_bytes(H: OracleH) -> dict:
     return dict(lowrank=lr, dense=dn, total=lr + dn, by_tag=by_tag)
 
 
-def ranks_only(P, kernel, scale, eps, eta, leaf, s, L_force=None):
-    """Partition + truncated-SVD ranks only (singular values, no vectors) — for storage
-    studies (Table 3) where factors are not needed.  Returns
-    (tree, partition, rank[], m[], n[]) with rank = -1 for blocks kept dense."""
+_RO = {}
+
+
+def _ro_init(P, perm, kernel, scale, eps):
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)  # one BLAS thread per worker process
+    _RO.update(P=P, perm=perm, kernel=kernel, scale=scale, eps=eps)
+
+
+def _ro_rank(job):
     from scipy.linalg import svdvals
     from .compress import truncation_rank
+    i0, i1, j0, j1 = job
+    A, _ = kernel_block(_RO["P"], _RO["perm"][i0:i1], _RO["perm"][j0:j1], _RO["kernel"], _RO["scale"])
+    return truncation_rank(svdvals(A), _RO["eps"])[0] if A.size else 0
+
+
+def ranks_only(P, kernel, scale, eps, eta, leaf, s, workers=None):
+    """Partition + truncated-SVD ranks only (singular values, no vectors) — for storage
+    studies (Table 3) where factors are not needed.  The independent
+    per-block SVDs are spread over worker processes.  Returns (tree, partition, rank[], m[],
+    n[]) with rank = -1 for blocks kept dense."""
+    import os
+    from concurrent.futures import ProcessPoolExecutor
     tr = build_tree(P, leaf)
     part = build_partition(tr, eta, s)
     nb = len(part)
     rank = np.full(nb, -1, np.int64)
     m = np.zeros(nb, np.int64)
     n = np.zeros(nb, np.int64)
+    jobs, idx = [], []
     for b in range(nb):
         l = int(part.level[b])
         i0, i1 = tr.cluster(l, int(part.tgt[b]))
@@ -206,6 +225,10 @@ def ranks_only(P, kernel, scale, eps, eta, leaf, s, L_force=None):
         m[b], n[b] = i1 - i0, j1 - j0
         if part.kind[b] in (DIAG, LNBR):
             continue
-        A, _ = kernel_block(P, tr.perm[i0:i1], tr.perm[j0:j1], kernel, scale)
-        rank[b] = truncation_rank(svdvals(A), eps)[0] if A.size else 0
+        jobs.append((i0, i1, j0, j1))
+        idx.append(b)
+    with ProcessPoolExecutor(max_workers=workers or os.cpu_count(), initializer=_ro_init,
+                             initargs=(P, tr.perm, kernel, scale, eps)) as ex:
+        for b, r in zip(idx, ex.map(_ro_rank, jobs, chunksize=64)):
+            rank[b] = r
     return tr, part, rank, m, n
