@@ -20,7 +20,8 @@ import parity_lib as PL  # noqa: E402
 from paper_2604_09147_b200 import hh  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SMALL = ["2d_tiny", "2d_fig8_e4", "2d_fig8_e2", "3d_small_inv_r", "3d_small_exp", "3d_sphere_small", "2d_circle_small"]
+SMALL = ["2d_tiny", "2d_fig8_e4", "2d_fig8_e2", "3d_small_inv_r", "3d_small_exp", "3d_sphere_small", "2d_circle_small",
+         "1d_log"]
 
 
 @pytest.fixture(scope="module", params=SMALL)
@@ -56,7 +57,7 @@ def test_check1c_packing_function(built):
 def test_check2_matvec_vs_oracle_on_exported_factors(built):
     _, cfg, P, H, ex, Ho = built
     lay = PL.check_packing(ex)
-    for nrhs in sorted({1, cfg["nrhs"], 3, 16}):
+    for nrhs in sorted({1, cfg["nrhs"], 3, 16, 20}):   # 20 = a 16-column chunk + a 4-column chunk
         x = W.make_rhs(cfg, nrhs)
         y = PL.gpu_matvec(H, x)
         yo = PL.oracle_matvec_on_export(ex, lay, x)

@@ -90,6 +90,9 @@ SMALL_CONFIGS = {
                            eps=1e-6, pset=P_MIXED, nrhs=1, xdist="normal"),
     "3d_small_exp": dict(k=13, N=8000, d=3, kernel=K_EXP, scale=0.1, leaf=64, eta=1.0, s=2,
                          eps=1e-6, pset=P_MIXED, nrhs=4, xdist="normal"),
+    # d = 1 (binary tree; the method is stated for any d)
+    "1d_log": dict(k=16, N=2000, d=1, kernel=K_LOG, scale=1.0, leaf=32, eta=1.0, s=2,
+                   eps=1e-8, pset=P_MIXED, nrhs=1, xdist="uniform_pm1"),
     # NEXT-4: points on the unit sphere (App. D) — most
     # leaf boxes empty, unbalanced occupancy (reading G20: empty clusters are skipped)
     "3d_sphere_small": dict(k=14, N=8000, d=3, kernel=K_INV_R, scale=1.0, leaf=64, eta=1.0, s=3,
