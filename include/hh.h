@@ -73,6 +73,11 @@ enum { HH_TAG_FP64 = 0, HH_TAG_FP32 = 1, HH_TAG_FP16 = 2, HH_TAG_BF16 = 3 };
  * (hh_matvec then returns HH_EINVAL).  Used for storage ratios of configurations that do
  * not fit in HBM (uniform-fp64 H_s at N = 2^20). */
 #define HH_LEDGER_ONLY (1u << 16)
+/* OR into precision_set (NEXT-3, bits-aware tie rule): when Eq. 4.4 admits bf16 it also admits
+ * fp16 (smaller u, same 16 bits); the paper keeps the largest u (bf16) —
+ * with this flag the block is stored in fp16 (3 more mantissa bits) unless an entry would
+ * overflow fp16, in which case bf16 stays.  Requires both HH_P_FP16 and HH_P_BF16. */
+#define HH_TIE_FP16 (1u << 17)
 
 /* switch_level: 0..L is Eq. 3.1 read literally (0 = HODLR); HH_SWITCH_NONE = pure H_s
  * (Alg. 1 with ell = L: dense leaf neighbours; in mixed precision a leaf neighbour is stored

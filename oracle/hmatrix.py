@@ -30,6 +30,7 @@ from .partition import DIAG, LNBR, SWITCH_NONE, Partition, build_partition
 from .tree import Tree, build_tree
 
 LR, DENSE = 0, 1
+TIE_FP16 = 1 << 17   # precision_set flag (include/hh.h HH_TIE_FP16): fp16 over bf16 when both qualify
 
 
 def choose_tag(nb2: float, norm2: float, eps: float, d: int, l: int, pset: int) -> tuple[int, bool]:
@@ -152,6 +153,9 @@ def build(P, kernel, scale, eps, eta, leaf, s, pset, keep_exact=False) -> Oracle
         H.tag_margin[b] = abs(tm)
         H.fallback += int(fb)
         maxabs = max(float(np.max(np.abs(U))) if U.size else 0.0, H.maxabs_w[b])
+        if (pset & TIE_FP16) and tag == F.BF16 and (pset & F.TAG_BIT[F.FP16]) and \
+                not np.isinf(F.round_rne(np.array([maxabs]), F.FP16)[0]):
+            tag = F.FP16   # NEXT-3 bits-aware tie rule: same 16 bits, 3 more mantissa bits
         tag, pr = guard_tag(tag, maxabs, pset)
         H.promoted += int(pr)
         p = int(H.rank[b])

@@ -154,7 +154,7 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
   if (leaf_size < 1) return fail(HH_EINVAL, "leaf_size must be >= 1");
   if (leaf_size > 256) return fail(HH_EUNSUPPORTED, "leaf_size > 256 not supported by this build");
   if (!(precision_set & HH_P_FP64)) return fail(HH_EINVAL, "precision_set must contain HH_P_FP64");
-  if (precision_set & ~(0xFu | HH_LEDGER_ONLY)) return fail(HH_EINVAL, "unknown precision_set bits");
+  if (precision_set & ~(0xFu | HH_LEDGER_ONLY | HH_TIE_FP16)) return fail(HH_EINVAL, "unknown precision_set bits");
   if (kernel.kind < 0 || kernel.kind > 4) return fail(HH_EINVAL, "unknown kernel kind");
   if ((kernel.kind == HH_K_GAUSS || kernel.kind == HH_K_EXP) && !(kernel.scale > 0.0))
     return fail(HH_EINVAL, "kernel scale must be > 0");
@@ -175,6 +175,7 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
     H->s = switch_level;
     H->pset = precision_set & 0xF;
     H->ledger = (precision_set & HH_LEDGER_ONLY) != 0;
+    H->tie16 = (precision_set & HH_TIE_FP16) && (precision_set & HH_P_FP16) && (precision_set & HH_P_BF16);
     DBuf pts;
     build_tree(H, points, st, pts);                                   // a1
     HH_REQUIRE(switch_level == HH_SWITCH_NONE || switch_level <= H->L, HH_EINVAL, "switch_level > L");

@@ -87,6 +87,7 @@ struct hh_matrix {
   int32_t leaf_size = 0;
   uint32_t pset = 0;
   bool ledger = false;
+  bool tie16 = false;   // HH_TIE_FP16
   int64_t ncell = 0;
   // tree
   std::vector<int64_t> leaf_start;        // host copy [ncell+1]

@@ -57,6 +57,8 @@ void assign_tags(hh_matrix *H) {
       }
     }
     fb += !found;
+    // NEXT-3 tie rule: fp16 instead of bf16 (same bits, smaller u) unless fp16 would overflow
+    if (H->tie16 && tag == TAG_BF16 && H->maxabs[b] < kOverflow[TAG_FP16]) tag = TAG_FP16;
     // range guard: promote while the largest factor entry would overflow the format
     while (tag != TAG_FP64 && H->maxabs[b] >= kOverflow[tag]) {
       int nt = tag == TAG_BF16 ? TAG_FP16 : tag == TAG_FP16 ? TAG_FP32 : TAG_FP64;

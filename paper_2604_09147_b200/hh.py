@@ -19,6 +19,7 @@ K_LOG, K_INV_R, K_INV_R2, K_GAUSS, K_EXP = range(5)
 P_FP64, P_FP32, P_FP16, P_BF16 = 1, 2, 4, 8
 P_MIXED = 15
 LEDGER_ONLY = 1 << 16
+TIE_FP16 = 1 << 17
 SWITCH_NONE = -1
 ARENA_W, ARENA_U, ARENA_D = 0, 4, 8
 

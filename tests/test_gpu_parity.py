@@ -280,3 +280,22 @@ def test_switch_level_search_matches_oracle():
     ell_g, by_g = hh.hh_switch_level_search(Pd, *args)
     assert len(by_g) == L + 2
     assert ell_g == ell_o and by_g == by_o, (ell_g, ell_o, by_g, by_o)
+
+
+def test_tie_rule_parity():
+    """NEXT-3 HH_TIE_FP16: same partition, ranks, tags (fp16 where the paper's rule says
+    bf16), packing and matvec as the oracle with the same flag."""
+    cfg = dict(W.SMALL_CONFIGS["2d_fig8_e2"])
+    cfg["pset"] = cfg["pset"] | W.TIE_FP16
+    P = W.make_points(cfg)
+    H = PL.gpu_build(P, cfg)
+    ex = PL.export(H)
+    Ho = PL.oracle_build(P, cfg)
+    PL.check_partition(ex, Ho)
+    bad_r, bad_t, st = PL.rank_tag_parity(ex, Ho)
+    assert bad_r == 0 and bad_t == 0, st
+    B = ex["blocks"]
+    assert np.sum((B["storage"] == 0) & (B["tag"] == 3)) == 0 and np.sum(B["tag"] == 2) > 0
+    lay = PL.check_packing(ex)
+    x = W.make_rhs(cfg, 2)
+    assert PL.rel2(PL.gpu_matvec(H, x), PL.oracle_matvec_on_export(ex, lay, x)) <= 1e-12

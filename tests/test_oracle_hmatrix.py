@@ -317,3 +317,25 @@ def test_table3_s1_over_s2_3d_inv_r():
     ratio = S1 / S2
     print("Table 3 L=3 eps=1e-6: S1/S2 =", ratio)
     assert 1.45 <= ratio <= 1.75, ratio
+
+
+def test_tie_rule_fp16_over_bf16():
+    """NEXT-3 bits-aware tie rule (HH_TIE_FP16): every block the paper's rule stores in bf16
+    (largest u) goes to fp16 instead — same bits, so identical storage —
+    unless an entry would overflow fp16; the blocks' rounding errors can only shrink."""
+    cfg = W.SMALL_CONFIGS["2d_fig8_e2"]
+    P = W.make_points(cfg)
+    args = (P, cfg["kernel"], cfg["scale"], cfg["eps"], cfg["eta"], cfg["leaf"], cfg["s"])
+    H0 = HM.build(*args, cfg["pset"], keep_exact=True)
+    H1 = HM.build(*args, cfg["pset"] | HM.TIE_FP16, keep_exact=True)
+    lr = H0.storage == HM.LR
+    assert np.sum(H0.tag[lr] == F.BF16) > 0
+    moved = lr & (H0.tag == F.BF16)
+    assert np.all(H1.tag[moved] == F.FP16)
+    assert np.all(H1.tag[lr & ~moved] == H0.tag[lr & ~moved])
+    assert HM.stored_bytes(H1)["total"] == HM.stored_bytes(H0)["total"]
+    for b in np.nonzero(moved)[0][:50]:
+        U, Wf = H1.exact[b]
+        e0 = np.linalg.norm(U @ Wf.T - H0.factors[b][0] @ H0.factors[b][1].T)
+        e1 = np.linalg.norm(U @ Wf.T - H1.factors[b][0] @ H1.factors[b][1].T)
+        assert e1 <= e0

@@ -23,6 +23,7 @@ KERNEL_NAMES = {K_LOG: "log", K_INV_R: "inv_r", K_INV_R2: "inv_r2", K_GAUSS: "ga
 # precision-set bitmask — identical to include/hh.h
 P_FP64, P_FP32, P_FP16, P_BF16 = 1, 2, 4, 8
 P_MIXED = P_FP64 | P_FP32 | P_FP16 | P_BF16
+TIE_FP16 = 1 << 17      # precision_set flag: bits-aware fp16-over-bf16 tie rule (NEXT-3)
 SWITCH_NONE = -1
 
 
