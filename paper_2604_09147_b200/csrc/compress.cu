@@ -202,17 +202,27 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double (*red)[NV], do
 
 // ---------------------------------------------------------------- Householder QR
 // A (m x k, col-major, ld m) in place: R in the upper triangle, reflector vectors below.
-template <bool FORM_Q>
-__global__ void __launch_bounds__(THREADS) k_qr(CBlk *blks, double *ws, int which) {
-  CBlk &B = blks[blockIdx.x];
+// SMEM: the m x k panel is copied to shared memory, factored there and (FORM_Q) turned into
+// Q in place (the dorg2r order: j = k-1 .. 0), then written back once — every Householder
+// step then costs shared-memory instead of L2 latency.  Used when m k doubles fit.
+constexpr int QR_SMEM_ELEMS = 13824;  // 108 KiB: two CTAs per SM
+template <bool FORM_Q, bool SMEM>
+__global__ void __launch_bounds__(THREADS) k_qr(CBlk *blks, const int32_t *__restrict__ order, double *ws, int which) {
+  extern __shared__ double qsm[];
+  CBlk &B = blks[order[blockIdx.x]];
   const int m = which == 0 ? B.m : B.n;
   const int k = B.k;
-  double *A = ws + (which == 0 ? B.oy : B.ozc);
+  double *Ag = ws + (which == 0 ? B.oy : B.ozc);
+  double *A = SMEM ? qsm : Ag;
   double *tau = ws + B.otau;
   __shared__ double red[THREADS / 32][8];
   __shared__ double bc[8];
   __shared__ double sc[4];
   const int tid = threadIdx.x;
+  if (SMEM) {
+    for (int64_t e = tid; e < (int64_t)m * k; e += THREADS) A[e] = Ag[e];
+    __syncthreads();
+  }
   for (int j = 0; j < k; ++j) {
     double *aj = A + (int64_t)j * m;
     double v1[1] = {0.0};
@@ -260,6 +270,44 @@ __global__ void __launch_bounds__(THREADS) k_qr(CBlk *blks, double *ws, int whic
       }
     }
     __syncthreads();
+  }
+  if (SMEM) {
+    if (FORM_Q) {
+      // in place: A <- H_0 ... H_{k-1} [I; 0] (reflector j lives below the diagonal of column j)
+      for (int j = k - 1; j >= 0; --j) {
+        const double t = tau[j];
+        for (int c0 = j + 1; c0 < k; c0 += 8) {  // apply H_j to columns j+1.. (rows j..m)
+          const int nc = min(8, k - c0);
+          double w[8] = {};
+          for (int i = j + 1 + tid; i < m; i += THREADS) {
+            const double v = A[(int64_t)j * m + i];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (q < nc) w[q] = __fma_rn(v, A[(int64_t)(c0 + q) * m + i], w[q]);
+          }
+          block_sum<8>(w, red, bc, nc);
+          if (tid < nc) bc[tid] = t * (bc[tid] + A[(int64_t)(c0 + tid) * m + j]);
+          __syncthreads();
+          for (int i = j + tid; i < m; i += THREADS) {
+            const double v = (i == j) ? 1.0 : A[(int64_t)j * m + i];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (q < nc) A[(int64_t)(c0 + q) * m + i] -= v * bc[q];
+          }
+          __syncthreads();
+        }
+        for (int i = tid; i < m; i += THREADS) {  // column j of Q
+          double *a = A + (int64_t)j * m;
+          a[i] = i < j ? 0.0 : (i == j ? 1.0 - t : -t * a[i]);
+        }
+        __syncthreads();
+      }
+      double *Q = ws + B.oq;
+      for (int64_t e = tid; e < (int64_t)m * k; e += THREADS) Q[e] = A[e];
+    } else {
+      for (int64_t e = tid; e < (int64_t)m * k; e += THREADS) Ag[e] = A[e];
+    }
+    return;
   }
   if (!FORM_Q) return;
   // explicit Q = H_0 ... H_{k-1} [I; 0] by backward accumulation (into oq)
@@ -613,6 +661,47 @@ __global__ void __launch_bounds__(THREADS) k_factors(CBlk *blks, const double *w
 }  // namespace
 
 // --------------------------------------------------------------------- host driver
+// QR launches: blocks whose panel fits shared memory take the SMEM kernel (one launch sized to
+// the largest of them), the rest the global-memory kernel.
+static void launch_qr(const std::vector<CBlk> &blks, int nb, DBuf &ordb, int which, CBlk *db, double *ws,
+                      cudaStream_t st) {
+  std::vector<int32_t> ord;
+  int nsm = 0;
+  int64_t mk_max = 0;
+  for (int i = 0; i < nb; ++i) {
+    const int64_t mk = (int64_t)(which == 0 ? blks[i].m : blks[i].n) * blks[i].k;
+    if (mk <= QR_SMEM_ELEMS) {
+      ord.push_back(i);
+      ++nsm;
+      mk_max = std::max(mk_max, mk);
+    }
+  }
+  for (int i = 0; i < nb; ++i) {
+    const int64_t mk = (int64_t)(which == 0 ? blks[i].m : blks[i].n) * blks[i].k;
+    if (mk > QR_SMEM_ELEMS) ord.push_back(i);
+  }
+  h2d(ordb, ord, st);
+  const int32_t *od = ordb.as<int32_t>();
+  if (nsm > 0) {
+    const size_t sm = sizeof(double) * (size_t)mk_max;
+    if (which == 0) {
+      HH_CUDA(cudaFuncSetAttribute(k_qr<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * QR_SMEM_ELEMS)));
+      k_qr<true, true><<<nsm, THREADS, sm, st>>>(db, od, ws, which);
+    } else {
+      HH_CUDA(cudaFuncSetAttribute(k_qr<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * QR_SMEM_ELEMS)));
+      k_qr<false, true><<<nsm, THREADS, sm, st>>>(db, od, ws, which);
+    }
+    HH_LAUNCHED();
+  }
+  if (nb - nsm > 0) {
+    if (which == 0)
+      k_qr<true, false><<<nb - nsm, THREADS, 0, st>>>(db, od + nsm, ws, which);
+    else
+      k_qr<false, false><<<nb - nsm, THREADS, 0, st>>>(db, od + nsm, ws, which);
+    HH_LAUNCHED();
+  }
+}
+
 KernelFn make_kernel_fn(const hh_kernel &kk) {
   KernelFn K{};
   K.kind = kk.kind;
@@ -646,7 +735,7 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
   res.assign(jobs.size(), CompressResult{});
   const KernelFn K = make_kernel_fn(H->kernel);
   const double delta = 1e-9;
-  DBuf wsb, blkb, taskb, partb, ordb;
+  DBuf wsb, blkb, taskb, partb, ordb, ordq_y, ordq_z;
   size_t ws_cap = 0;
   size_t pos = 0;
   std::vector<CBlk> blks;
@@ -734,8 +823,7 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
       HH_LAUNCHED();
     }
     mark(1);
-    k_qr<true><<<nb, THREADS, 0, st>>>(db, ws, 0);
-    HH_LAUNCHED();
+    launch_qr(blks, nb, ordq_y, 0, db, ws, st);
     mark(2);
     // Z = A^T Q (and a copy for the R-only QR)
     for (size_t t0 = 0; t0 < tB.size(); t0 += 65535) {
@@ -747,15 +835,15 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
       HH_LAUNCHED();
     }
     mark(3);
-    k_qr<false><<<nb, THREADS, 0, st>>>(db, ws, 1);
-    HH_LAUNCHED();
+    launch_qr(blks, nb, ordq_z, 1, db, ws, st);
     mark(4);
     {
-      // k-buckets: (k <= 32: 256 threads), (<= 64: 512), (<= 168: 1024, smem), (> 168: global)
+      // k-buckets: (k <= 32: 256 threads), (<= 64: 512), (<= 96: 512), (<= 168: 1024, smem),
+      // (> 168: 1024, global) — small cores get small CTAs / smem so several share an SM
       std::vector<int32_t> ord;
-      int cnt[4] = {0, 0, 0, 0}, kmx[4] = {0, 0, 0, 0};
-      auto bucket = [](int k) { return k <= 32 ? 0 : k <= 64 ? 1 : k <= JAC_SMEM_K ? 2 : 3; };
-      for (int bkt = 0; bkt < 4; ++bkt)
+      int cnt[5] = {0, 0, 0, 0, 0}, kmx[5] = {0, 0, 0, 0, 0};
+      auto bucket = [](int k) { return k <= 32 ? 0 : k <= 64 ? 1 : k <= 96 ? 2 : k <= JAC_SMEM_K ? 3 : 4; };
+      for (int bkt = 0; bkt < 5; ++bkt)
         for (int i = 0; i < nb; ++i)
           if (bucket(blks[i].k) == bkt) {
             ord.push_back(i);
@@ -765,13 +853,14 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
       h2d(ordb, ord, st);
       const int32_t *od = ordb.as<int32_t>();
       int start = 0;
-      for (int bkt = 0; bkt < 4; ++bkt) {
+      for (int bkt = 0; bkt < 5; ++bkt) {
         if (cnt[bkt] == 0) continue;
         const int jsm = std::min(kmx[bkt], JAC_SMEM_K);
-        const size_t jsmem = bkt == 3 ? 0 : sizeof(double) * (size_t)jsm * jsm;
+        const size_t jsmem = bkt == 4 ? 0 : sizeof(double) * (size_t)jsm * jsm;
         if (bkt == 0) {
           k_jacobi<256><<<cnt[bkt], 256, jsmem, st>>>(db, od + start, ws);
-        } else if (bkt == 1) {
+        } else if (bkt <= 2) {
+          HH_CUDA(cudaFuncSetAttribute(k_jacobi<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * 96 * 96)));
           k_jacobi<512><<<cnt[bkt], 512, jsmem, st>>>(db, od + start, ws);
         } else {
           HH_CUDA(cudaFuncSetAttribute(k_jacobi<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
