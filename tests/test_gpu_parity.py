@@ -299,3 +299,16 @@ def test_tie_rule_parity():
     lay = PL.check_packing(ex)
     x = W.make_rhs(cfg, 2)
     assert PL.rel2(PL.gpu_matvec(H, x), PL.oracle_matvec_on_export(ex, lay, x)) <= 1e-12
+
+
+def test_host_buffer_entry_point_matches_device_path():
+    """hh_matvec_host (the e2e path bench.py times: H2D of x, matvec, D2H of y on the stream)
+    returns bitwise the device-buffer result, for nrhs = 1 and a 16 + 4 chunked 20."""
+    cfg = W.SMALL_CONFIGS["3d_small_exp"]
+    P = W.make_points(cfg)
+    H = PL.gpu_build(P, cfg)
+    for nrhs in (1, 20):
+        x = W.make_rhs(cfg, nrhs)
+        yd = PL.gpu_matvec(H, x)
+        yh = hh.hh_matvec_host(H, np.asfortranarray(x))
+        assert np.array_equal(np.asarray(yh).reshape(yd.shape, order="F"), yd)
