@@ -83,7 +83,7 @@ __device__ __forceinline__ double entry(const KernelFn &K, const double *pts, in
 // mode 1: Z[:, c] = sum_i A(i, j) Q(i, c)       rows = source cluster, cols = target
 constexpr int GT_M = 64, GT_K = 16;
 
-// GT_N = sketch columns per CTA tile (32 or 64, chosen per batch from its widest sketch)
+// GT_N = sketch columns per CTA tile (32, 48 or 64: blocks are launched by sketch-width bucket)
 template <int MODE, int GT_N>
 __global__ void __launch_bounds__(THREADS) k_gemm_gen(const Task *__restrict__ tasks, CBlk *blks, double *ws,
                                                       const double *__restrict__ pts, int64_t N, int d, KernelFn K) {
@@ -148,11 +148,16 @@ __global__ void __launch_bounds__(THREADS) k_gemm_gen(const Task *__restrict__ t
         a[q] = t.x;
         a[q + 1] = t.y;
       }
+      if constexpr (TC % 2 == 0) {
 #pragma unroll
-      for (int q = 0; q < TC; q += 2) {
-        const double2 t = *reinterpret_cast<const double2 *>(&Xs[jj][tx * TC + q]);
-        x[q] = t.x;
-        x[q + 1] = t.y;
+        for (int q = 0; q < TC; q += 2) {
+          const double2 t = *reinterpret_cast<const double2 *>(&Xs[jj][tx * TC + q]);
+          x[q] = t.x;
+          x[q + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < TC; ++q) x[q] = Xs[jj][tx * TC + q];
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r)
@@ -787,10 +792,22 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
     }
     const int nb = (int)blks.size();
     // tasks: target-row tiles (mode 0 / resid), source-row tiles (mode 1)
+    // GEMM tasks grouped by sketch-width bucket (k <= 32, <= 48, > 48: 64-column tiles)
     std::vector<Task> tA, tB, tR;
+    int nA[3] = {0, 0, 0}, nB[3] = {0, 0, 0}, kmxb[3] = {0, 0, 0};
+    auto kb = [](int k) { return k <= 32 ? 0 : k <= 48 ? 1 : 2; };
+    for (int bkt = 0; bkt < 3; ++bkt)
+      for (int i = 0; i < nb; ++i) {
+        if (kb(blks[i].k) != bkt) continue;
+        kmxb[bkt] = std::max(kmxb[bkt], blks[i].k);
+        for (int r = 0; r < blks[i].m; r += GT_M, ++nA[bkt]) tA.push_back(Task{i, r});
+      }
+    for (int bkt = 0; bkt < 3; ++bkt)
+      for (int i = 0; i < nb; ++i) {
+        if (kb(blks[i].k) != bkt) continue;
+        for (int r = 0; r < blks[i].n; r += GT_M, ++nB[bkt]) tB.push_back(Task{i, r});
+      }
     for (int i = 0; i < nb; ++i) {
-      for (int r = 0; r < blks[i].m; r += GT_M) tA.push_back(Task{i, r});
-      for (int r = 0; r < blks[i].n; r += GT_M) tB.push_back(Task{i, r});
       blks[i].task0 = (int64_t)tR.size();
       for (int r = 0; r < blks[i].m; r += RT_M) tR.push_back(Task{i, r});
     }
@@ -805,35 +822,38 @@ void run_compress(hh_matrix *H, const double *pts, const std::vector<CompressJob
     all.insert(all.end(), tR.begin(), tR.end());
     h2d(taskb, all, st);
     partb.alloc(sizeof(double) * 2 * std::max<size_t>(1, tR.size()));
-    int kmax = 0;
-    for (auto &c : blks) kmax = std::max(kmax, c.k);
-    const bool narrow = kmax <= 32;  // 32-column tiles when every sketch of the batch fits
-    const int gy = narrow ? 1 : (kmax + 63) / 64;
     const Task *dA = taskb.as<Task>(), *dB = dA + tA.size(), *dR = dB + tB.size();
     double *ws = wsb.as<double>();
     CBlk *db = blkb.as<CBlk>();
+    // fused entry GEMMs per sketch-width bucket (MODE 0: Y = A Omega, MODE 1: Z = A^T Q)
+    auto gemm = [&](int mode, const Task *tasks, const int *cnt) {
+      size_t base = 0;
+      for (int bkt = 0; bkt < 3; ++bkt) {
+        const int gy = bkt < 2 ? 1 : (kmxb[2] + 63) / 64;
+        for (size_t t0 = 0; t0 < (size_t)cnt[bkt]; t0 += 65535) {
+          dim3 g((unsigned)std::min<size_t>(65535, cnt[bkt] - t0), gy);
+          const Task *tp = tasks + base + t0;
+          if (mode == 0) {
+            if (bkt == 0) k_gemm_gen<0, 32><<<g, THREADS, 0, st>>>(tp, db, ws, pts, H->N, H->d, K);
+            else if (bkt == 1) k_gemm_gen<0, 48><<<g, THREADS, 0, st>>>(tp, db, ws, pts, H->N, H->d, K);
+            else k_gemm_gen<0, 64><<<g, THREADS, 0, st>>>(tp, db, ws, pts, H->N, H->d, K);
+          } else {
+            if (bkt == 0) k_gemm_gen<1, 32><<<g, THREADS, 0, st>>>(tp, db, ws, pts, H->N, H->d, K);
+            else if (bkt == 1) k_gemm_gen<1, 48><<<g, THREADS, 0, st>>>(tp, db, ws, pts, H->N, H->d, K);
+            else k_gemm_gen<1, 64><<<g, THREADS, 0, st>>>(tp, db, ws, pts, H->N, H->d, K);
+          }
+          HH_LAUNCHED();
+        }
+        base += cnt[bkt];
+      }
+    };
     mark(0);
-    // Y = A Omega
-    for (size_t t0 = 0; t0 < tA.size(); t0 += 65535) {
-      dim3 g((unsigned)std::min<size_t>(65535, tA.size() - t0), gy);
-      if (narrow)
-        k_gemm_gen<0, 32><<<g, THREADS, 0, st>>>(dA + t0, db, ws, pts, H->N, H->d, K);
-      else
-        k_gemm_gen<0, 64><<<g, THREADS, 0, st>>>(dA + t0, db, ws, pts, H->N, H->d, K);
-      HH_LAUNCHED();
-    }
+    gemm(0, dA, nA);
     mark(1);
     launch_qr(blks, nb, ordq_y, 0, db, ws, st);
     mark(2);
     // Z = A^T Q (and a copy for the R-only QR)
-    for (size_t t0 = 0; t0 < tB.size(); t0 += 65535) {
-      dim3 g((unsigned)std::min<size_t>(65535, tB.size() - t0), gy);
-      if (narrow)
-        k_gemm_gen<1, 32><<<g, THREADS, 0, st>>>(dB + t0, db, ws, pts, H->N, H->d, K);
-      else
-        k_gemm_gen<1, 64><<<g, THREADS, 0, st>>>(dB + t0, db, ws, pts, H->N, H->d, K);
-      HH_LAUNCHED();
-    }
+    gemm(1, dB, nB);
     mark(3);
     launch_qr(blks, nb, ordq_z, 1, db, ws, st);
     mark(4);
