@@ -302,6 +302,9 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
   } catch (const std::exception &e) {
     delete H;
     return fail(HH_ECUDA, e.what());
+  } catch (...) {
+    delete H;
+    return fail(HH_ECUDA, "unexpected error");
   }
 }
 
@@ -318,6 +321,12 @@ hh_status hh_matvec(hh_handle H, const double *x, double *y, int32_t nrhs, void 
     return HH_OK;
   } catch (const Error &e) {
     return fail(e.st, e.what());
+  } catch (const std::bad_alloc &) {
+    return fail(HH_ENOMEM, "host allocation failed");
+  } catch (const std::exception &e) {
+    return fail(HH_ECUDA, e.what());
+  } catch (...) {
+    return fail(HH_ECUDA, "unexpected error");
   }
 }
 
@@ -340,6 +349,12 @@ hh_status hh_matvec_host(hh_handle H, const double *x_host, double *y_host, int3
     return HH_OK;
   } catch (const Error &e) {
     return fail(e.st, e.what());
+  } catch (const std::bad_alloc &) {
+    return fail(HH_ENOMEM, "host allocation failed");
+  } catch (const std::exception &e) {
+    return fail(HH_ECUDA, e.what());
+  } catch (...) {
+    return fail(HH_ECUDA, "unexpected error");
   }
 }
 
@@ -370,6 +385,12 @@ hh_status hh_matvec_timing(hh_handle H, double *ms, int64_t *count) {
     return HH_OK;
   } catch (const Error &e) {
     return fail(e.st, e.what());
+  } catch (const std::bad_alloc &) {
+    return fail(HH_ENOMEM, "host allocation failed");
+  } catch (const std::exception &e) {
+    return fail(HH_ECUDA, e.what());
+  } catch (...) {
+    return fail(HH_ECUDA, "unexpected error");
   }
 }
 
@@ -426,6 +447,12 @@ hh_status hh_export(hh_handle H, hh_export_t *out) {
     return HH_OK;
   } catch (const Error &e) {
     return fail(e.st, e.what());
+  } catch (const std::bad_alloc &) {
+    return fail(HH_ENOMEM, "host allocation failed");
+  } catch (const std::exception &e) {
+    return fail(HH_ECUDA, e.what());
+  } catch (...) {
+    return fail(HH_ECUDA, "unexpected error");
   }
 }
 
@@ -492,6 +519,12 @@ hh_status hh_selftest_round(const double *host_in, int64_t n, int32_t tag, uint3
     return HH_OK;
   } catch (const Error &e) {
     return fail(e.st, e.what());
+  } catch (const std::bad_alloc &) {
+    return fail(HH_ENOMEM, "host allocation failed");
+  } catch (const std::exception &e) {
+    return fail(HH_ECUDA, e.what());
+  } catch (...) {
+    return fail(HH_ECUDA, "unexpected error");
   }
 }
 
