@@ -12,3 +12,4 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(gather|ph
 ncu --set full --clock-control none --import-source on -k regex:k_phase -s 6 -c 2 -o gpurun_out/prof \
     python bench.py > gpurun_out/ncu_full.log 2>&1; echo "bench/ncu rc $?"
 python bench.py --nrhs 16 --no-cpu-baseline > gpurun_out/bench_nrhs16.log 2>&1; echo "bench16 rc $?"
+# 4. (optional, ~15 min) BASELINE config 4 sweep + ledger-only storage baselines: bash scripts/run_sweep.sh
