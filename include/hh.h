@@ -230,6 +230,24 @@ const char *hh_last_error(void);
  * n host doubles; host_bits receives the target bit patterns (RNE, single rounding, G16). */
 hh_status hh_selftest_round(const double *host_in, int64_t n, int32_t tag, uint32_t *host_bits);
 
+/*
+ * Test hooks on the library's host-side C++ (no device needed; used by the CPU test suite):
+ *   hh_selftest_partition — the block partition (partition.cpp: Eq. 3.1 expansion, canonical
+ *     order) of a tree given by its leaf offsets leaf_start[2^{dL}+1].  Writes up to
+ *     `capacity` blocks (level, kind, tgt, src) and the total count to *nblocks (HH_EINVAL if
+ *     capacity is too small: call with capacity 0 to size).
+ *   hh_selftest_layout — the packing function (layout.cpp) for given blocks,
+ *     ranks, tags and storage kinds: every offset hh_export reports, u_leaf_off[4*(ncell+1)],
+ *     d_leaf_off[ncell+1] and w_bytes[4].
+ */
+hh_status hh_selftest_partition(const int64_t *leaf_start, int32_t d, int32_t L, double eta, int32_t switch_level,
+                                int64_t capacity, int64_t *nblocks, uint8_t *level, uint8_t *kind, int64_t *tgt,
+                                int64_t *src);
+hh_status hh_selftest_layout(const int64_t *leaf_start, int32_t d, int32_t L, int64_t nblocks, const uint8_t *level,
+                             const int64_t *tgt, const int64_t *src, const int32_t *rank, const uint8_t *tag,
+                             const uint8_t *storage, int64_t *zoff, int64_t *w_off, int64_t *wcol, int64_t *ucol,
+                             int64_t *d_off, int64_t *u_leaf_off, int64_t *d_leaf_off, int64_t *w_bytes);
+
 /* Number of kernels the library enqueued since load (launch accounting for bench.py). */
 int64_t hh_kernel_launches(void);
 

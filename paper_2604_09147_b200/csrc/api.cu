@@ -503,6 +503,78 @@ hh_status hh_free(hh_handle H) {
   return HH_OK;
 }
 
+hh_status hh_selftest_partition(const int64_t *leaf_start, int32_t d, int32_t L, double eta, int32_t switch_level,
+                                int64_t capacity, int64_t *nblocks, uint8_t *level, uint8_t *kind, int64_t *tgt,
+                                int64_t *src) {
+  g_err.clear();
+  if (!leaf_start || !nblocks || d < 1 || d > 3 || L < 0 || d * L > 26 || !(eta > 0))
+    return fail(HH_EINVAL, "bad argument");
+  try {
+    hh_matrix H;
+    H.d = d;
+    H.L = L;
+    H.s = switch_level;
+    H.eta = eta;
+    H.ncell = 1ll << (d * L);
+    H.leaf_start.assign(leaf_start, leaf_start + H.ncell + 1);
+    build_partition(&H);
+    const int64_t nb = (int64_t)H.level.size();
+    *nblocks = nb;
+    if (capacity < nb) return capacity == 0 ? HH_OK : fail(HH_EINVAL, "capacity too small");
+    for (int64_t b = 0; b < nb; ++b) {
+      if (level) level[b] = H.level[b];
+      if (kind) kind[b] = H.kind[b];
+      if (tgt) tgt[b] = H.tgt[b];
+      if (src) src[b] = H.src[b];
+    }
+    return HH_OK;
+  } catch (const Error &e) {
+    return fail(e.st, e.what());
+  } catch (...) {
+    return fail(HH_EINVAL, "partition failed");
+  }
+}
+
+hh_status hh_selftest_layout(const int64_t *leaf_start, int32_t d, int32_t L, int64_t nblocks, const uint8_t *level,
+                             const int64_t *tgt, const int64_t *src, const int32_t *rank, const uint8_t *tag,
+                             const uint8_t *storage, int64_t *zoff, int64_t *w_off, int64_t *wcol, int64_t *ucol,
+                             int64_t *d_off, int64_t *u_leaf_off, int64_t *d_leaf_off, int64_t *w_bytes) {
+  g_err.clear();
+  if (!leaf_start || !level || !tgt || !src || !rank || !tag || !storage || nblocks < 0 || d < 1 || d > 3 || L < 0 ||
+      d * L > 26)
+    return fail(HH_EINVAL, "bad argument");
+  try {
+    hh_matrix H;
+    H.d = d;
+    H.L = L;
+    H.ncell = 1ll << (d * L);
+    H.leaf_start.assign(leaf_start, leaf_start + H.ncell + 1);
+    H.level.assign(level, level + nblocks);
+    H.tgt.assign(tgt, tgt + nblocks);
+    H.src.assign(src, src + nblocks);
+    H.rank.assign(rank, rank + nblocks);
+    H.tag.assign(tag, tag + nblocks);
+    H.storage.assign(storage, storage + nblocks);
+    compute_layout(&H);
+    for (int64_t b = 0; b < nblocks; ++b) {
+      if (zoff) zoff[b] = H.zoff[b];
+      if (w_off) w_off[b] = H.w_off[b];
+      if (wcol) wcol[b] = H.wcol[b];
+      if (ucol) ucol[b] = H.ucol[b];
+      if (d_off) d_off[b] = H.d_off[b];
+    }
+    if (u_leaf_off) std::copy(H.u_leaf_off.begin(), H.u_leaf_off.end(), u_leaf_off);
+    if (d_leaf_off) std::copy(H.d_leaf_off.begin(), H.d_leaf_off.end(), d_leaf_off);
+    if (w_bytes)
+      for (int g = 0; g < 4; ++g) w_bytes[g] = H.w_bytes[g];
+    return HH_OK;
+  } catch (const Error &e) {
+    return fail(e.st, e.what());
+  } catch (...) {
+    return fail(HH_EINVAL, "layout failed");
+  }
+}
+
 /* Test hook: apply the device storage-rounding routine of `tag` (1..3) to host values and
  * return the bit patterns (checked against the oracle's definition-based rounding). */
 hh_status hh_selftest_round(const double *host_in, int64_t n, int32_t tag, uint32_t *host_bits) {

@@ -86,6 +86,9 @@ def _load():
     lib.hh_free.argtypes = [C.c_void_p]
     lib.hh_last_error.restype = C.c_char_p
     lib.hh_kernel_launches.restype = C.c_int64
+    lib.hh_selftest_partition.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int64,
+                                          C.POINTER(C.c_int64), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.hh_selftest_layout.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64] + [C.c_void_p] * 14
     lib.hh_switch_level_search.argtypes = [C.c_void_p, C.c_int64, C.c_int32, hh_kernel, C.c_double, C.c_double,
                                            C.c_int32, C.c_uint32, C.c_void_p, C.POINTER(C.c_int32),
                                            C.POINTER(C.c_int32), C.c_void_p, C.c_int32]
@@ -93,7 +96,8 @@ def _load():
     lib.hh_matvec_profile.argtypes = [C.c_void_p, C.c_int32]
     lib.hh_matvec_timing.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     for f in ("hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_selftest_round",
-              "hh_matvec_profile", "hh_matvec_timing", "hh_switch_level_search"):
+              "hh_matvec_profile", "hh_matvec_timing", "hh_switch_level_search", "hh_selftest_partition",
+              "hh_selftest_layout"):
         getattr(lib, f).restype = C.c_int
     return lib
 
@@ -101,7 +105,7 @@ def _load():
 lib = _load()
 EXPORTED = ["hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_last_error",
             "hh_kernel_launches", "hh_selftest_round", "hh_matvec_profile", "hh_matvec_timing",
-            "hh_switch_level_search"]
+            "hh_switch_level_search", "hh_selftest_partition", "hh_selftest_layout"]
 
 
 def _check(st):
@@ -229,6 +233,42 @@ def hh_switch_level_search(points, kernel: int, scale: float, eps: float, eta: f
                                       leaf_size, precision_set, _stream_ptr(stream), C.byref(lvl), C.byref(L),
                                       buf.ctypes.data, buf.size))
     return int(lvl.value), buf[:L.value + 2].tolist()
+
+
+def selftest_partition(leaf_start: np.ndarray, d: int, L: int, eta: float, switch_level: int) -> dict:
+    """Host-side partition of the library (no device): blocks of the tree with these leaf offsets."""
+    ls = np.ascontiguousarray(leaf_start, dtype=np.int64)
+    nb = C.c_int64()
+    _check(lib.hh_selftest_partition(ls.ctypes.data, d, L, eta, switch_level, 0, C.byref(nb), None, None, None, None))
+    n = nb.value
+    out = dict(level=np.empty(n, np.uint8), kind=np.empty(n, np.uint8), tgt=np.empty(n, np.int64),
+               src=np.empty(n, np.int64))
+    _check(lib.hh_selftest_partition(ls.ctypes.data, d, L, eta, switch_level, n, C.byref(nb), out["level"].ctypes.data,
+                                     out["kind"].ctypes.data, out["tgt"].ctypes.data, out["src"].ctypes.data))
+    return out
+
+
+def selftest_layout(leaf_start, d, L, level, tgt, src, rank, tag, storage) -> dict:
+    """Host-side packing function of the library (no device) for given blocks."""
+    ls = np.ascontiguousarray(leaf_start, dtype=np.int64)
+    lv = np.ascontiguousarray(level, dtype=np.uint8)
+    tg = np.ascontiguousarray(tgt, dtype=np.int64)
+    sr = np.ascontiguousarray(src, dtype=np.int64)
+    rk = np.ascontiguousarray(rank, dtype=np.int32)
+    ta = np.ascontiguousarray(tag, dtype=np.uint8)
+    st = np.ascontiguousarray(storage, dtype=np.uint8)
+    nb, ncell = lv.size, ls.size - 1
+    out = {k: np.empty(nb, np.int64) for k in ("zoff", "w_off", "wcol", "ucol", "d_off")}
+    out["u_leaf_off"] = np.empty(4 * (ncell + 1), np.int64)
+    out["d_leaf_off"] = np.empty(ncell + 1, np.int64)
+    out["w_bytes"] = np.empty(4, np.int64)
+    _check(lib.hh_selftest_layout(ls.ctypes.data, d, L, nb, lv.ctypes.data, tg.ctypes.data, sr.ctypes.data,
+                                  rk.ctypes.data, ta.ctypes.data, st.ctypes.data, out["zoff"].ctypes.data,
+                                  out["w_off"].ctypes.data, out["wcol"].ctypes.data, out["ucol"].ctypes.data,
+                                  out["d_off"].ctypes.data, out["u_leaf_off"].ctypes.data,
+                                  out["d_leaf_off"].ctypes.data, out["w_bytes"].ctypes.data))
+    out["u_leaf_off"] = out["u_leaf_off"].reshape(4, -1)
+    return out
 
 
 def hh_free(H: Handle):
