@@ -110,7 +110,7 @@ def build(P, kernel, scale, eps, eta, leaf, s, pset, keep_exact=False) -> Oracle
     H.margin = np.full(nb, np.inf)
     H.maxabs_w = np.zeros(nb)
     H.tag_margin = np.full(nb, np.inf)
-    mixed = pset != F.TAG_BIT[F.FP64]
+    mixed = (pset & 0xF) != F.TAG_BIT[F.FP64]   # format bits only (flags such as TIE_FP16 excluded)
     perm = tree.perm
     exact = {}
     # Alg. 1 + Alg. 4: compress every admissible block, norms from singular values
