@@ -16,7 +16,9 @@
  *   - Alg. 4: ||H~||^2 from the kept singular values
  *   - Alg. 2 / Eq. 4.4: per-block storage precision, the largest u in the precision set with
  *     u <= eps / (2^{dl/2} xi), xi = ||H~_IJ||/||H~||
- * and packs the factors into per-precision HBM arenas (layout: DESIGN.md §4).
+ * and packs the factors into per-precision HBM arenas (layout: DESIGN.md §4).  hh_build runs
+ * libhh's own kernels and, for large blocks with wide sketches only, cuBLAS DGEMM and
+ * cuSOLVER QR/SVD (compress_big.cu); hh_matvec runs only libhh's sm_100a kernels.
  *
  * Conventions shared by every entry point
  *   - Pointers documented as "device" must be cudaMalloc'd (or torch CUDA) memory on the
