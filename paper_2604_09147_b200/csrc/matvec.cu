@@ -53,6 +53,20 @@ constexpr int THREADS = NCT + 32;      // + one producer warp
 #ifndef HH_MV_STAGES
 #define HH_MV_STAGES 2
 #endif
+#ifndef HH_MV_P2STAGES
+#define HH_MV_P2STAGES HH_MV_STAGES  // phase-2 ring depth at NR = 16
+#endif
+#ifndef HH_MV_P2X
+#define HH_MV_P2X 0  // phase-2 z bytes per stage at NR = 16 (0: sized for the smallest leaves)
+#endif
+// DMMA K-loops without per-step bounds checks (tail step peeled): measured ~1% faster in
+// phase 1, ~2% slower in phase 2 (profiles/r01_variants.txt)
+#ifndef HH_MV_PEEL1
+#define HH_MV_PEEL1 1
+#endif
+#ifndef HH_MV_PEEL2
+#define HH_MV_PEEL2 0
+#endif
 constexpr int META = 64;
 
 // FP64 tensor-core (DMMA m8n8k4) consumers for the multi-RHS contractions (NR = 8, 16):
@@ -69,11 +83,13 @@ template <int NR, int PH> struct Geo {  // PH = phase (1: x~ rows per W row wind
   // vector bytes per stage: phase 1 needs one NR-vector per W row (a 248-column row is >= 1 KiB
   // of factors), phase 2 one per U column (|R| rows, as little as ~32 elements)
   static constexpr int XDATA =
-      NR <= 2 ? HH_MV_XDATA : (PH == 1 ? (NR * 512 > 4096 ? NR * 512 : 4096) : NR * 2048 / (32768 / WDATA));
+      NR <= 2 ? HH_MV_XDATA
+              : (PH == 1 ? (NR * 512 > 4096 ? NR * 512 : 4096)
+                         : ((NR >= 16 && HH_MV_P2X > 0) ? HH_MV_P2X : NR * 2048 / (32768 / WDATA)));
   static constexpr int XELEMS = XDATA / 8;                        // doubles (rows x NR)
   static constexpr int XBUF = XDATA + 32;
   static constexpr int STAGE = WBUF + XBUF + META;
-  static constexpr int STAGES = HH_MV_STAGES;
+  static constexpr int STAGES = (PH == 2 && NR >= 16) ? HH_MV_P2STAGES : HH_MV_STAGES;
   static constexpr size_t red_bytes() {  // phase-2 cross-group reduction buffer
     return use_mma<NR>() ? sizeof(double) * NCW * 4 * (NR / 8) * 32 * 2 : sizeof(double) * NCT * NR * (NR >= 8 ? 2 : 1);
   }
@@ -292,8 +308,28 @@ __device__ __forceinline__ void p1_mma_rows_t(const uint8_t *wst, const double *
   bool cv[MT];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) cv[mt] = col0 + mt * 8 + mq < ct;
+  int k0 = 0;
+#if HH_MV_PEEL1
+  if (col0 + MT * 8 <= ct) {
+    const int kfull = nrows & ~3;
 #pragma unroll 2
-  for (int k0 = 0; k0 < nrows; k0 += 4) {
+    for (; k0 < kfull; k0 += 4) {
+      const int row = k0 + kq;
+      double b[NR / 8];
+#pragma unroll
+      for (int nt = 0; nt < NR / 8; ++nt) b[nt] = xst[row * NR + nt * 8 + mq];
+      const T *wrow = W + row * ct + col0 + mq;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const double av = up<TAG>(wrow[mt * 8]);
+#pragma unroll
+        for (int nt = 0; nt < NR / 8; ++nt) dmma(c[mt][nt], av, b[nt]);
+      }
+    }
+  }
+#endif
+#pragma unroll 2
+  for (; k0 < nrows; k0 += 4) {
     const int row = k0 + kq;
     const bool rv = row < nrows;
     double b[NR / 8];
@@ -548,8 +584,30 @@ __device__ __forceinline__ void p2_mma_cols_t(const uint8_t *ust, const double *
   bool rv[MT];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) rv[mt] = row0 + mt * 8 + mq < nr;
+  int k0 = 4 * kfirst;
+#if HH_MV_PEEL2
+  // whole K-steps: no column checks; rows checked only when the group's last tile is ragged
+  const bool rows_full = row0 + MT * 8 <= nr;
+  const int kfull = ncols & ~3;
+  if (rows_full) {
 #pragma unroll 2
-  for (int k0 = 4 * kfirst; k0 < ncols; k0 += 4 * KS) {
+    for (; k0 < kfull; k0 += 4 * KS) {
+      const int col = k0 + kq;
+      double b[NR / 8];
+#pragma unroll
+      for (int nt = 0; nt < NR / 8; ++nt) b[nt] = zst[col * NR + nt * 8 + mq];
+      const T *ucol = U + col * nr + row0 + mq;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const double av = up<TAG>(ucol[mt * 8]);
+#pragma unroll
+        for (int nt = 0; nt < NR / 8; ++nt) dmma(c[mt][nt], av, b[nt]);
+      }
+    }
+  }
+#endif
+#pragma unroll 2
+  for (; k0 < ncols; k0 += 4 * KS) {
     const int col = k0 + kq;
     const bool cvl = col < ncols;
     double b[NR / 8];
