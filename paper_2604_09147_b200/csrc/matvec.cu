@@ -48,7 +48,7 @@ constexpr int THREADS = NCT + 32;      // + one producer warp
 #define HH_MV_XDATA 4096
 #endif
 #ifndef HH_MV_P2HI
-#define HH_MV_P2HI 16384   // phase 2 at NR = 16: 16 KiB stages fit 2 CTAs/SM (measured faster)
+#define HH_MV_P2HI 28672   // phase 2 at NR = 16: 28 KiB factor + 28 KiB z stages, 2 CTAs/SM (measured)
 #endif
 #ifndef HH_MV_STAGES
 #define HH_MV_STAGES 2
@@ -57,10 +57,13 @@ constexpr int THREADS = NCT + 32;      // + one producer warp
 #define HH_MV_P2STAGES HH_MV_STAGES  // phase-2 ring depth at NR = 16
 #endif
 #ifndef HH_MV_P2X
-#define HH_MV_P2X 0  // phase-2 z bytes per stage at NR = 16 (0: sized for the smallest leaves)
+#define HH_MV_P2X 28672  // phase-2 z bytes per stage at NR = 16 (0: NR * 2048 / (32768 / P2HI))
 #endif
 // DMMA K-loops without per-step bounds checks (tail step peeled): measured ~1% faster in
 // phase 1, ~2% slower in phase 2 (profiles/r01_variants.txt)
+#ifndef HH_MV_P2ALIAS
+#define HH_MV_P2ALIAS 1  // phase 2 at NR = 16: the leaf-end reduction reuses the leaf's last stage
+#endif
 #ifndef HH_MV_PEEL1
 #define HH_MV_PEEL1 1
 #endif
@@ -90,11 +93,13 @@ template <int NR, int PH> struct Geo {  // PH = phase (1: x~ rows per W row wind
   static constexpr int XBUF = XDATA + 32;
   static constexpr int STAGE = WBUF + XBUF + META;
   static constexpr int STAGES = (PH == 2 && NR >= 16) ? HH_MV_P2STAGES : HH_MV_STAGES;
+  // phase 2 at NR = 16 may reduce in the leaf's last stage (held until the reduction ends)
+  static constexpr bool RED_IN_STAGE = PH == 2 && NR >= 16 && HH_MV_P2ALIAS && use_mma<NR>();
   static constexpr size_t red_bytes() {  // phase-2 cross-group reduction buffer
     return use_mma<NR>() ? sizeof(double) * NCW * 4 * (NR / 8) * 32 * 2 : sizeof(double) * NCT * NR * (NR >= 8 ? 2 : 1);
   }
   static constexpr size_t smem(bool red) {
-    return (size_t)STAGES * STAGE + 2 * STAGES * sizeof(uint64_t) + (red ? red_bytes() : 0);
+    return (size_t)STAGES * STAGE + 2 * STAGES * sizeof(uint64_t) + (red && !RED_IN_STAGE ? red_bytes() : 0);
   }
 };
 
@@ -683,8 +688,14 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
       while (kbase >= KS) kbase -= KS;
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (!G::RED_IN_STAGE || !(m.flags & 1))
+      if (lane == 0) mbar_arrive(&empty[s]);
     if (m.flags & 1) {
+      if constexpr (G::RED_IN_STAGE) {
+        static_assert(G::red_bytes() <= (size_t)G::WBUF + G::XBUF, "reduction fits the stage data");
+        red = reinterpret_cast<double *>(smem + s * G::STAGE);
+        consumer_sync();  // every warp is done with the stage's U / z before it is overwritten
+      }
       double *mine = red + (size_t)warp * 4 * NT * 64;
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
@@ -715,7 +726,10 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
         a.y[i + col * a.ldy] = s0;
         a.y[i + (col + 1) * a.ldy] = s1;
       }
+      if constexpr (G::RED_IN_STAGE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       consumer_sync();
+      if constexpr (G::RED_IN_STAGE)
+        if (lane == 0) mbar_arrive(&empty[s]);  // the stage goes back to the producer's TMA
       kbase = 0;
     }
   }

@@ -1,10 +1,9 @@
-# Time the phase-2 NR=16 variants (scripts/variants_p2.sh) with CUDA events, two rounds.
+# A/B of the phase-2 NR=16 stage geometry: adopted default vs the previous one (libhh_p2old).
 cd "$(dirname "$0")/.."
-mkdir -p gpurun_out
 for r in 1 2; do
-  for v in default alias_s2_w24 alias_s2_w28_x24 alias_s2_w32_x20 alias_s2_w24_x32 alias_s2_w28_x28; do
+  for v in default p2old; do
     if [ "$v" = default ]; then lib=paper_2604_09147_b200/libhh.so; else lib=paper_2604_09147_b200/libhh_$v.so; fi
-    for c in "3d_exp_proxy 16" "3d_laplace 16" "3d_sphere 16"; do
+    for c in "3d_exp_proxy 16" "3d_laplace 16" "3d_sphere 16" "3d_laplace 20"; do
       HH_LIB=$PWD/$lib timeout 300 python scripts/profile_matvec.py $c 3 2>&1 | grep nrhs= | sed "s/^/[$v] /"
     done
   done
