@@ -50,6 +50,12 @@ constexpr int THREADS = NCT + 32;      // + one producer warp
 #ifndef HH_MV_P2HI
 #define HH_MV_P2HI 28672   // phase 2 at NR = 16: 28 KiB factor + 28 KiB z stages, 2 CTAs/SM (measured)
 #endif
+#ifndef HH_MV_P1HI
+#define HH_MV_P1HI 49152  // phase-1 factor bytes per stage at NR = 16 (48 KiB + 8 KiB x~, 2 CTAs/SM, measured)
+#endif
+#ifndef HH_MV_P1X
+#define HH_MV_P1X 8192  // phase-1 x~ bytes per stage at NR = 16 (0: max(NR * 512, 4096))
+#endif
 #ifndef HH_MV_STAGES
 #define HH_MV_STAGES 2
 #endif
@@ -81,13 +87,13 @@ template <int NR> constexpr bool use_mma() { return HH_MV_MMA && (NR == 8 || NR 
 
 template <int NR, int PH> struct Geo {  // PH = phase (1: x~ rows per W row window, 2: z per U column)
   // factor bytes per stage (phase 2 at NR >= 8 may use smaller stages to fit 2 CTAs/SM)
-  static constexpr int WDATA = (PH == 2 && NR >= 16) ? HH_MV_P2HI : HH_MV_WDATA;
+  static constexpr int WDATA = (PH == 2 && NR >= 16) ? HH_MV_P2HI : (PH == 1 && NR >= 16) ? HH_MV_P1HI : HH_MV_WDATA;
   static constexpr int WBUF = WDATA + 32;                            // + 16-B alignment slack
   // vector bytes per stage: phase 1 needs one NR-vector per W row (a 248-column row is >= 1 KiB
   // of factors), phase 2 one per U column (|R| rows, as little as ~32 elements)
   static constexpr int XDATA =
       NR <= 2 ? HH_MV_XDATA
-              : (PH == 1 ? (NR * 512 > 4096 ? NR * 512 : 4096)
+              : (PH == 1 ? ((NR >= 16 && HH_MV_P1X > 0) ? HH_MV_P1X : (NR * 512 > 4096 ? NR * 512 : 4096))
                          : ((NR >= 16 && HH_MV_P2X > 0) ? HH_MV_P2X : NR * 2048 / (32768 / WDATA)));
   static constexpr int XELEMS = XDATA / 8;                        // doubles (rows x NR)
   static constexpr int XBUF = XDATA + 32;
