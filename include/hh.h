@@ -103,8 +103,12 @@ enum { HH_STORE_LR = 0, HH_STORE_DENSE = 1 };
  *   precision_set bitmask of HH_P_*, must contain HH_P_FP64; may OR HH_LEDGER_ONLY.
  *   cuda_stream   cudaStream_t (NULL = legacy default stream).  hh_build synchronises it.
  *   out           receives the handle on HH_OK (unchanged otherwise).
- * Errors: HH_EUNSUPPORTED if a block's truncated-SVD rank needs a sketch wider than 4096
- * columns (the device compressor's limit), HH_EINVAL (bad argument), HH_ENUMERIC (non-finite point or kernel entry, e.g.
+ * Sketch limit: the device compressor widens a block's randomized sketch until its rank decision
+ * provably equals the truncated-SVD decision (G26).  If a block reaches the 4096-column
+ * limit (below min(|I|, |J|)) with a decision that is valid (the explicit residual meets eps) but
+ * not proved minimal, the rank is accepted and counted in hh_info_t.n_inexact.
+ * Errors: HH_EUNSUPPORTED if a block's rank exceeds 4096 columns (no sketch of <= 4096 columns
+ * meets eps), or a whole-GPU-path block needs more device memory than is free, HH_EINVAL (bad argument), HH_ENUMERIC (non-finite point or kernel entry, e.g.
  * log of a zero distance between distinct points is mapped to 0 and counted — not an
  * error — but an overflowing entry is), HH_EDEPTH, HH_ENOMEM (arenas exceed free HBM),
  * HH_ECUDA.
@@ -182,6 +186,8 @@ typedef struct {
   int32_t c_far, c_nbr, c_sib;/* measured sparsity constants (max blocks per target) */
   int64_t n_fallback, n_promoted, n_coincident, n_retry;
   double build_seconds;
+  int64_t n_inexact;          /* blocks whose rank decision could not be proved equal to the truncated-SVD
+                                 rank within the 4096-column sketch limit (accepted; see hh_build) */
 } hh_info_t;
 
 hh_status hh_info(hh_handle H, hh_info_t *info);
@@ -249,6 +255,19 @@ hh_status hh_selftest_layout(const int64_t *leaf_start, int32_t d, int32_t L, in
                              const int64_t *tgt, const int64_t *src, const int32_t *rank, const uint8_t *tag,
                              const uint8_t *storage, int64_t *zoff, int64_t *w_off, int64_t *wcol, int64_t *ucol,
                              int64_t *d_off, int64_t *u_leaf_off, int64_t *d_leaf_off, int64_t *w_bytes);
+
+/*
+ * hh_selftest_tags — the library's host-side Alg. 4 norm + Alg. 2 / Eq. 4.4 tagging (layout.cpp:
+ * assign_tags: squared exact form, range guard, HH_TIE_FP16, PAPER.md:992 beneficial rule) on
+ * given per-block ranks, ||H~_b||^2 (nb2), ||H_b||^2 (tot) and factor max |entry| (maxabs), with the
+ * storage kinds hh_build starts from (diagonal dense; leaf neighbours dense in uniform precision).
+ * Outputs tag[], storage[], rank[] (in/out: 0 for neighbours the beneficial rule keeps dense),
+ * *norm2 = ||H~||^2 and counts[0] = n_fallback, counts[1] = n_promoted.  No device needed.
+ */
+hh_status hh_selftest_tags(const int64_t *leaf_start, int32_t d, int32_t L, int64_t nblocks, const uint8_t *level,
+                          const uint8_t *kind, const int64_t *tgt, const int64_t *src, int32_t *rank,
+                          const double *nb2, const double *tot, const double *maxabs, double eps,
+                          uint32_t precision_set, uint8_t *tag, uint8_t *storage, double *norm2, int64_t *counts);
 
 /* Number of kernels the library enqueued since load (launch accounting for bench.py). */
 int64_t hh_kernel_launches(void);

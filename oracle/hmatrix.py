@@ -56,6 +56,71 @@ def guard_tag(tag: int, maxabs: float, pset: int) -> tuple[int, bool]:
     return order[i], promoted
 
 
+def alg4_norm2(kind, nb2, tot) -> float:
+    """Alg. 4: ||H~||^2 = sum of trace(Sigma~^2) over low-rank blocks + the
+    direct ||H_IJ||^2 of dense leaf blocks (and, for ell = L, of the leaf neighbours,
+    PAPER.md:1354-1362), summed in canonical block order."""
+    norm2 = 0.0
+    for b in range(len(kind)):
+        norm2 += float(tot[b]) if int(kind[b]) in (DIAG, LNBR) else float(nb2[b])
+    return norm2
+
+
+def tag_blocks(d, level, kind, m, n, rank, nb2, tot, maxabs, eps, pset) -> dict:
+    """Alg. 2 over a block table: Eq. 4.4 tag (choose_tag), the bits-aware tie rule when
+    TIE_FP16 is set, the range guard (guard_tag) and, for pure H_s in mixed precision, the
+    PAPER.md:992 beneficial rule for leaf neighbours.  Blocks start dense when they are leaf
+    diagonals, or leaf neighbours in uniform precision (Alg. 1 keeps them dense); every other
+    block is a compressed low-rank candidate.  ``maxabs`` = max |entry| of the block's
+    unrounded factors U and W.  Returns per-block tag / storage / rank (0 for dense), the
+    pre-rule rank and tag of every low-rank candidate (lr_rank, lr_tag), ||H~||^2, the
+    fallback / promoted counts and each tag decision's relative distance from its threshold."""
+    nb = len(kind)
+    mixed = (pset & 0xF) != F.TAG_BIT[F.FP64]
+    norm2 = alg4_norm2(kind, nb2, tot)
+    tag = np.zeros(nb, np.int64)
+    lr_tag = np.full(nb, -1, np.int64)
+    storage = np.full(nb, LR, np.int64)
+    out_rank = np.array(rank, dtype=np.int64).copy()
+    lr_rank = np.full(nb, -1, np.int64)
+    tag_margin = np.full(nb, np.inf)
+    fallback = promoted = 0
+    rhs = eps * eps * norm2
+    for b in range(nb):
+        k, l = int(kind[b]), int(level[b])
+        if k == DIAG or (k == LNBR and not mixed):
+            storage[b] = DENSE
+            out_rank[b] = 0
+            continue
+        t, fb = choose_tag(float(nb2[b]), norm2, eps, d, l, pset)
+        # distance of the decision from the threshold (for parity tolerances)
+        u = F.unit_roundoff(t)
+        lhs = (u * u) * 2.0 ** (d * l) * float(nb2[b])
+        tm = (rhs - lhs) / rhs if rhs else np.inf
+        if t != F.BF16:  # also distance to qualifying for the next larger u
+            nxt = [c for c in (F.FP32, F.FP16, F.BF16) if F.unit_roundoff(c) > u and (pset & F.TAG_BIT[c])]
+            if nxt:
+                un = min(F.unit_roundoff(c) for c in nxt)
+                tm = min(abs(tm), abs(((un * un) * 2.0 ** (d * l) * float(nb2[b]) - rhs) / rhs))
+        tag_margin[b] = abs(tm)
+        fallback += int(fb)
+        if (pset & TIE_FP16) and t == F.BF16 and (pset & F.TAG_BIT[F.FP16]) and \
+                not np.isinf(F.round_rne(np.array([maxabs[b]]), F.FP16)[0]):
+            t = F.FP16   # NEXT-3 bits-aware tie rule: same 16 bits, 3 more mantissa bits
+        t, pr = guard_tag(t, float(maxabs[b]), pset)
+        promoted += int(pr)
+        lr_rank[b], lr_tag[b] = int(rank[b]), t
+        if k == LNBR:
+            # PAPER.md:992 beneficial rule (mixed pure H_s only): low-rank iff fewer bits
+            if not (int(rank[b]) * (int(m[b]) + int(n[b])) * F.BITS[t] < int(m[b]) * int(n[b]) * 64):
+                storage[b] = DENSE
+                out_rank[b] = 0
+                continue
+        tag[b] = t
+    return dict(tag=tag, storage=storage, rank=out_rank, lr_rank=lr_rank, lr_tag=lr_tag, norm2=norm2,
+                fallback=fallback, promoted=promoted, tag_margin=tag_margin)
+
+
 @dataclass
 class OracleH:
     tree: Tree
@@ -83,6 +148,8 @@ class OracleH:
     fallback: int = 0
     promoted: int = 0
     coincident: int = 0
+    lr_rank: np.ndarray = None    # rank / tag of every compressed candidate before the beneficial rule
+    lr_tag: np.ndarray = None
 
     def rows(self, b):
         l = int(self.part.level[b])
@@ -129,44 +196,23 @@ def build(P, kernel, scale, eps, eta, leaf, s, pset, keep_exact=False) -> Oracle
         H.tot[b] = c["tot"]
         H.maxabs_w[b] = float(np.max(np.abs(c["W"]))) if c["p"] else 0.0
         exact[b] = (c["U"], c["W"], A)
-    # ||H~||^2 (Alg. 4): low-rank blocks by trace(Sigma~^2); dense and (ell = L) leaf
-    # neighbours by their direct norm.
-    norm2 = 0.0
-    for b in range(nb):
-        kind = int(part.kind[b])
-        norm2 += H.tot[b] if kind in (DIAG, LNBR) else H.nb2[b]
-    H.norm2 = norm2
-    # Alg. 2: tag every low-rank block
+    m = np.array([H.rows(b)[1] - H.rows(b)[0] for b in range(nb)], np.int64)
+    n = np.array([H.rows(b)[3] - H.rows(b)[2] for b in range(nb)], np.int64)
+    maxabs = np.zeros(nb)
     for b, (U, W, A) in exact.items():
-        l = int(part.level[b])
-        tag, fb = choose_tag(H.nb2[b], norm2, eps, tree.d, l, pset)
-        # distance of the decision from the threshold (for parity tolerances)
-        u = F.unit_roundoff(tag)
-        lhs = (u * u) * 2.0 ** (tree.d * l) * H.nb2[b]
-        rhs = eps * eps * norm2
-        tm = (rhs - lhs) / rhs if rhs else np.inf
-        if tag != F.BF16:  # also distance to qualifying for the next larger u
-            nxt = [t for t in (F.FP32, F.FP16, F.BF16) if F.unit_roundoff(t) > u and (pset & F.TAG_BIT[t])]
-            if nxt:
-                un = min(F.unit_roundoff(t) for t in nxt)
-                tm = min(abs(tm), abs(((un * un) * 2.0 ** (tree.d * l) * H.nb2[b] - rhs) / rhs))
-        H.tag_margin[b] = abs(tm)
-        H.fallback += int(fb)
-        maxabs = max(float(np.max(np.abs(U))) if U.size else 0.0, H.maxabs_w[b])
-        if (pset & TIE_FP16) and tag == F.BF16 and (pset & F.TAG_BIT[F.FP16]) and \
-                not np.isinf(F.round_rne(np.array([maxabs]), F.FP16)[0]):
-            tag = F.FP16   # NEXT-3 bits-aware tie rule: same 16 bits, 3 more mantissa bits
-        tag, pr = guard_tag(tag, maxabs, pset)
-        H.promoted += int(pr)
-        p = int(H.rank[b])
-        i0, i1, j0, j1 = H.rows(b)
-        if part.kind[b] == LNBR:
-            # PAPER.md:992 beneficial rule (mixed pure H_s only)
-            if not (p * ((i1 - i0) + (j1 - j0)) * F.BITS[tag] < (i1 - i0) * (j1 - j0) * 64):
-                H.storage[b] = DENSE
-                H.dense[b] = A
-                H.rank[b] = 0
-                continue
+        maxabs[b] = max(float(np.max(np.abs(U))) if U.size else 0.0, H.maxabs_w[b])
+    T = tag_blocks(tree.d, part.level, part.kind, m, n, H.rank, H.nb2, H.tot, maxabs, eps, pset)
+    H.norm2 = T["norm2"]
+    H.tag_margin = T["tag_margin"]
+    H.fallback, H.promoted = T["fallback"], T["promoted"]
+    H.lr_rank, H.lr_tag = T["lr_rank"], T["lr_tag"]
+    for b, (U, W, A) in exact.items():
+        if T["storage"][b] == DENSE:       # PAPER.md:992 beneficial rule kept it dense
+            H.storage[b] = DENSE
+            H.dense[b] = A
+            H.rank[b] = 0
+            continue
+        tag = int(T["tag"][b])
         H.tag[b] = tag
         H.factors[b] = (F.round_rne(U, tag), F.round_rne(W, tag))
         if keep_exact:

@@ -22,20 +22,28 @@ from . import hmatrix as HM
 from .partition import SWITCH_NONE
 
 
+def walk(L: int, S_s: int, S_h) -> tuple[int, list]:
+    """Alg. 5's bottom-up walk given S_s and a callable S_h(ell) for
+    ell < L.  Returns (ell*, bytes) with bytes[l] = S_h(l) for the visited levels (-1
+    otherwise) and bytes[L] = bytes[L+1] = S_s."""
+    out = [-1] * (L + 2)
+    out[L] = out[L + 1] = S_s
+    ell, s = L, 0                       # S_1(L) - S_2(L) = 0: the ell = L branch is H_s
+    while ell > 0:
+        Sh = S_h(ell - 1)
+        out[ell - 1] = Sh
+        s_new = S_s - Sh                # S_1(ell-1) - S_2(ell-1)
+        if s_new <= s:
+            break
+        s, ell = s_new, ell - 1
+    return ell, out
+
+
 def alg_lstar(P, kernel, scale, eps, eta, leaf, pset):
     """Returns (ell*, L, bytes) with bytes[l] = S_h(l) for the visited levels (-1 otherwise)
     and bytes[L] = bytes[L+1] = S_s."""
     Hs = HM.build(P, kernel, scale, eps, eta, leaf, SWITCH_NONE, pset)
     L = Hs.tree.L
     Ss = HM.stored_bytes(Hs)["total"]
-    out = [-1] * (L + 2)
-    out[L] = out[L + 1] = Ss
-    ell, s = L, 0
-    while ell > 0:
-        Sh = HM.stored_bytes(HM.build(P, kernel, scale, eps, eta, leaf, ell - 1, pset))["total"]
-        out[ell - 1] = Sh
-        s_new = Ss - Sh
-        if s_new <= s:
-            break
-        s, ell = s_new, ell - 1
+    ell, out = walk(L, Ss, lambda l: HM.stored_bytes(HM.build(P, kernel, scale, eps, eta, leaf, l, pset))["total"])
     return ell, L, out

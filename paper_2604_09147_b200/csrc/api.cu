@@ -22,7 +22,6 @@ hh_status fail(hh_status s, const std::string &m) {
   return s;
 }
 
-constexpr int KMAX = 4096;  // sketch width limit (HODLR-level blocks at eps=1e-6 reach ranks of ~10^3)
 
 __global__ void k_round(const double *in, int64_t n, int tag, uint32_t *out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -79,7 +78,7 @@ void compress_all(hh_matrix *H, const double *pts, const std::vector<int64_t> &l
   std::vector<CompressJob> jobs;
   size_t pos = 0;
   const size_t batch = 16384;
-  int64_t retries = 0;
+  int64_t retries = 0, inexact = 0;
   std::vector<CompressJob> retry;
   std::vector<CompressResult> res;
   std::vector<std::vector<int>> cls_p(64 * 8);
@@ -111,6 +110,7 @@ void compress_all(hh_matrix *H, const double *pts, const std::vector<int64_t> &l
         continue;
       }
       HH_REQUIRE(r.p >= 0, HH_EUNSUPPORTED, "block rank exceeds the sketch limit (4096)");
+      inexact += !r.ok;  // at the sketch limit: valid (residual <= eps) but not proved minimal
       HH_REQUIRE(std::isfinite(r.tot) && std::isfinite(r.nb2), HH_ENUMERIC, "non-finite kernel entry");
       H->rank[b] = r.p;
       H->kfinal[b] = r.k;
@@ -129,6 +129,7 @@ void compress_all(hh_matrix *H, const double *pts, const std::vector<int64_t> &l
     }
   }
   H->info.n_retry = retries;
+  H->info.n_inexact = inexact;
 }
 
 }  // namespace
@@ -572,6 +573,53 @@ hh_status hh_selftest_layout(const int64_t *leaf_start, int32_t d, int32_t L, in
     return fail(e.st, e.what());
   } catch (...) {
     return fail(HH_EINVAL, "layout failed");
+  }
+}
+
+hh_status hh_selftest_tags(const int64_t *leaf_start, int32_t d, int32_t L, int64_t nblocks, const uint8_t *level,
+                          const uint8_t *kind, const int64_t *tgt, const int64_t *src, int32_t *rank,
+                          const double *nb2, const double *tot, const double *maxabs, double eps,
+                          uint32_t precision_set, uint8_t *tag, uint8_t *storage, double *norm2, int64_t *counts) {
+  g_err.clear();
+  if (!leaf_start || !level || !kind || !tgt || !src || !rank || !nb2 || !tot || !maxabs || !tag || !storage ||
+      !norm2 || !counts || nblocks < 0 || d < 1 || d > 3 || L < 0 || d * L > 26 || !(precision_set & HH_P_FP64))
+    return fail(HH_EINVAL, "bad argument");
+  try {
+    hh_matrix H;
+    H.d = d;
+    H.L = L;
+    H.eps = eps;
+    H.ncell = 1ll << (d * L);
+    H.leaf_start.assign(leaf_start, leaf_start + H.ncell + 1);
+    H.pset = precision_set & 0xF;
+    H.tie16 = (precision_set & HH_TIE_FP16) && (precision_set & HH_P_FP16) && (precision_set & HH_P_BF16);
+    H.level.assign(level, level + nblocks);
+    H.kind.assign(kind, kind + nblocks);
+    H.tgt.assign(tgt, tgt + nblocks);
+    H.src.assign(src, src + nblocks);
+    H.rank.assign(rank, rank + nblocks);
+    H.nb2.assign(nb2, nb2 + nblocks);
+    H.tot.assign(tot, tot + nblocks);
+    H.maxabs.assign(maxabs, maxabs + nblocks);
+    const bool mixed = H.pset != HH_P_FP64;  // as hh_build: dense = diagonal (+ leaf neighbours when uniform)
+    H.storage.assign(nblocks, STORE_LR);
+    H.tag.assign(nblocks, TAG_FP64);
+    for (int64_t b = 0; b < nblocks; ++b)
+      if (H.kind[b] == KIND_DIAG || (H.kind[b] == KIND_LNBR && !mixed)) H.storage[b] = STORE_DENSE;
+    assign_tags(&H);
+    for (int64_t b = 0; b < nblocks; ++b) {
+      tag[b] = H.tag[b];
+      storage[b] = H.storage[b];
+      rank[b] = H.rank[b];
+    }
+    *norm2 = H.norm2;
+    counts[0] = H.info.n_fallback;
+    counts[1] = H.info.n_promoted;
+    return HH_OK;
+  } catch (const Error &e) {
+    return fail(e.st, e.what());
+  } catch (...) {
+    return fail(HH_EINVAL, "tagging failed");
   }
 }
 

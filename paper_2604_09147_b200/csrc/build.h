@@ -6,6 +6,8 @@
 
 namespace hh {
 
+constexpr int KMAX = 4096;  // sketch width limit (HODLR-level blocks at eps=1e-6 reach ranks of ~10^3)
+
 struct CompressJob {
   int64_t block;  // index into the handle's block table
   int32_t k;      // sketch width

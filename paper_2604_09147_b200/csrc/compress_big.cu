@@ -197,6 +197,16 @@ void run_compress_big(hh_matrix *H, const double *pts, const CompressJob &job, b
   auto grow = [](DBuf &buf, size_t bytes) {
     if (buf.bytes < bytes) buf.alloc(bytes);
   };
+  {
+    // the block is held explicitly in HBM: refuse (instead of failing in cudaMalloc) when it
+    // and the sketch buffers do not fit in the free device memory
+    const size_t need = sizeof(double) * ((size_t)m * n + 4 * (size_t)n * k + (size_t)m * k + (size_t)k * k);
+    size_t held = c.A.bytes + c.Om.bytes + c.Q.bytes + c.Z.bytes + c.Zc.bytes + c.VT.bytes, fr = 0, tot = 0;
+    HH_CUDA(cudaMemGetInfo(&fr, &tot));
+    HH_REQUIRE(need <= fr + held, HH_EUNSUPPORTED,
+               "block " + std::to_string(m) + " x " + std::to_string(n) + " needs " +
+                   std::to_string(need >> 20) + " MiB for whole-GPU compression, more than the free device memory");
+  }
   grow(c.A, sizeof(double) * m * n);
   grow(c.Om, sizeof(double) * n * k);
   grow(c.Q, sizeof(double) * m * k);
@@ -292,7 +302,9 @@ void run_compress_big(hh_matrix *H, const double *pts, const CompressJob &job, b
     p = best;
   }
   res.p = p;
-  if (!res.ok || p <= 0) {
+  // a not-ok decision is retried with a wider sketch, except at the sketch limit where the
+  // caller accepts it (counted as inexact): its nb2 / maxabs must then be the real ones
+  if (p <= 0 || (!res.ok && k < KMAX)) {
     res.nb2 = 0.0;
     res.maxabs = 0.0;
     return;

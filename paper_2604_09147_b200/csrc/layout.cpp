@@ -20,13 +20,23 @@
 namespace hh {
 
 static const double kU[4] = {0x1p-53, 0x1p-24, 0x1p-11, 0x1p-8};
-static const double kOverflow[4] = {INFINITY, 0x1.ffffffp127, 65520.0, 0x1.fep127};  // |x| >= this rounds to inf
 static const uint32_t kBit[4] = {HH_P_FP64, HH_P_FP32, HH_P_FP16, HH_P_BF16};
 
 void cluster_range(const hh_matrix *H, int l, int64_t m, int64_t &a, int64_t &n) {
   const int sh = H->d * (H->L - l);
   a = H->leaf_start[m << sh];
   n = H->leaf_start[(m + 1) << sh] - a;
+}
+
+// Range guard (G16): does the single RNE rounding of |x| to format `tag` overflow to inf?  Decided
+// by the same rounding routine that stores the factors (common.cuh), not by a threshold table.
+static bool overflows(int tag, double x) {
+  switch (tag) {
+    case TAG_FP32: return (to_fp32_bits(x) & 0x7FFFFFFFu) == 0x7F800000u;
+    case TAG_FP16: return (to_fp16_bits(x) & 0x7FFFu) == 0x7C00u;
+    case TAG_BF16: return (to_bf16_bits(x) & 0x7FFFu) == 0x7F80u;
+    default: return false;
+  }
 }
 
 void assign_tags(hh_matrix *H) {
@@ -58,14 +68,17 @@ void assign_tags(hh_matrix *H) {
     }
     fb += !found;
     // NEXT-3 tie rule: fp16 instead of bf16 (same bits, smaller u) unless fp16 would overflow
-    if (H->tie16 && tag == TAG_BF16 && H->maxabs[b] < kOverflow[TAG_FP16]) tag = TAG_FP16;
-    // range guard: promote while the largest factor entry would overflow the format
-    while (tag != TAG_FP64 && H->maxabs[b] >= kOverflow[tag]) {
+    if (H->tie16 && tag == TAG_BF16 && !overflows(TAG_FP16, H->maxabs[b])) tag = TAG_FP16;
+    // range guard: promote while the largest factor entry would overflow the format (the
+    // promoted counter counts blocks, however many steps they take)
+    bool promoted = false;
+    while (tag != TAG_FP64 && overflows(tag, H->maxabs[b])) {
       int nt = tag == TAG_BF16 ? TAG_FP16 : tag == TAG_FP16 ? TAG_FP32 : TAG_FP64;
       while (nt != TAG_FP64 && !(H->pset & kBit[nt])) nt = nt == TAG_FP16 ? TAG_FP32 : TAG_FP64;
       tag = nt;
-      ++pr;
+      promoted = true;
     }
+    pr += promoted;
     H->tag[b] = (uint8_t)tag;
     if (H->kind[b] == KIND_LNBR && mixed) {
       int64_t i0, m, j0, n;

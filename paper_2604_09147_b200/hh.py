@@ -45,7 +45,7 @@ class hh_info_t(C.Structure):
         ("stored_bytes", C.c_int64), ("stored_bytes_tag", C.c_int64 * 5), ("padded_bytes", C.c_int64),
         ("c_far", C.c_int32), ("c_nbr", C.c_int32), ("c_sib", C.c_int32),
         ("n_fallback", C.c_int64), ("n_promoted", C.c_int64), ("n_coincident", C.c_int64), ("n_retry", C.c_int64),
-        ("build_seconds", C.c_double),
+        ("build_seconds", C.c_double), ("n_inexact", C.c_int64),
     ]
 
     def as_dict(self):
@@ -89,6 +89,8 @@ def _load():
     lib.hh_selftest_partition.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int64,
                                           C.POINTER(C.c_int64), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.hh_selftest_layout.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64] + [C.c_void_p] * 14
+    lib.hh_selftest_tags.argtypes = ([C.c_void_p, C.c_int32, C.c_int32, C.c_int64] + [C.c_void_p] * 8 +
+                                     [C.c_double, C.c_uint32] + [C.c_void_p] * 4)
     lib.hh_switch_level_search.argtypes = [C.c_void_p, C.c_int64, C.c_int32, hh_kernel, C.c_double, C.c_double,
                                            C.c_int32, C.c_uint32, C.c_void_p, C.POINTER(C.c_int32),
                                            C.POINTER(C.c_int32), C.c_void_p, C.c_int32]
@@ -97,7 +99,7 @@ def _load():
     lib.hh_matvec_timing.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     for f in ("hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_selftest_round",
               "hh_matvec_profile", "hh_matvec_timing", "hh_switch_level_search", "hh_selftest_partition",
-              "hh_selftest_layout"):
+              "hh_selftest_layout", "hh_selftest_tags"):
         getattr(lib, f).restype = C.c_int
     return lib
 
@@ -105,7 +107,7 @@ def _load():
 lib = _load()
 EXPORTED = ["hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_last_error",
             "hh_kernel_launches", "hh_selftest_round", "hh_matvec_profile", "hh_matvec_timing",
-            "hh_switch_level_search", "hh_selftest_partition", "hh_selftest_layout"]
+            "hh_switch_level_search", "hh_selftest_partition", "hh_selftest_layout", "hh_selftest_tags"]
 
 
 def _check(st):
@@ -269,6 +271,27 @@ def selftest_layout(leaf_start, d, L, level, tgt, src, rank, tag, storage) -> di
                                   out["d_leaf_off"].ctypes.data, out["w_bytes"].ctypes.data))
     out["u_leaf_off"] = out["u_leaf_off"].reshape(4, -1)
     return out
+
+
+def selftest_tags(leaf_start, d, L, level, kind, tgt, src, rank, nb2, tot, maxabs, eps, pset) -> dict:
+    """Host-side Alg. 4 norm + Alg. 2 tagging of the library (no device) for given blocks."""
+    ls = np.ascontiguousarray(leaf_start, dtype=np.int64)
+    a = dict(level=np.ascontiguousarray(level, dtype=np.uint8), kind=np.ascontiguousarray(kind, dtype=np.uint8),
+             tgt=np.ascontiguousarray(tgt, dtype=np.int64), src=np.ascontiguousarray(src, dtype=np.int64),
+             nb2=np.ascontiguousarray(nb2, dtype=np.float64), tot=np.ascontiguousarray(tot, dtype=np.float64),
+             maxabs=np.ascontiguousarray(maxabs, dtype=np.float64))
+    rk = np.array(rank, dtype=np.int32)
+    nb = rk.size
+    tag = np.empty(nb, np.uint8)
+    storage = np.empty(nb, np.uint8)
+    norm2 = C.c_double()
+    counts = np.zeros(2, np.int64)
+    _check(lib.hh_selftest_tags(ls.ctypes.data, d, L, nb, a["level"].ctypes.data, a["kind"].ctypes.data,
+                                a["tgt"].ctypes.data, a["src"].ctypes.data, rk.ctypes.data, a["nb2"].ctypes.data,
+                                a["tot"].ctypes.data, a["maxabs"].ctypes.data, eps, pset, tag.ctypes.data,
+                                storage.ctypes.data, C.byref(norm2), counts.ctypes.data))
+    return dict(tag=tag, storage=storage, rank=rk, norm2=norm2.value, n_fallback=int(counts[0]),
+                n_promoted=int(counts[1]))
 
 
 def hh_free(H: Handle):

@@ -66,3 +66,47 @@ def test_packing_function_matches_oracle(d, L, eta):
         np.testing.assert_array_equal(got["u_leaf_off"], ref["u_leaf_off"])
         np.testing.assert_array_equal(got["d_leaf_off"], ref["d_leaf_off"])
         np.testing.assert_array_equal(got["w_bytes"], ref["w_bytes"])
+
+
+@pytest.mark.parametrize("d,L,eta", [(2, 3, 1.0), (3, 2, 1.0), (1, 5, 1.0)])
+def test_tagging_matches_oracle(d, L, eta):
+    """Alg. 4 norm + Alg. 2 tags (Eq. 4.4 squared form, range guard, tie rule, PAPER.md:992
+    beneficial rule): the library's host C++ (layout.cpp assign_tags via hh_selftest_tags) equals
+    the oracle's tag_blocks on random block tables whose norms span every format's threshold
+    and whose factor maxima straddle every format's overflow boundary."""
+    from oracle import hmatrix as HM
+    rng = np.random.default_rng(11 * d + L)
+    tr = _tree(d, L, rng, p_empty=0.2, mean=7)
+    edges = [65504.0, 65519.99, 65520.0, float.fromhex("0x1.fep127"), float.fromhex("0x1.ffp127"),
+             float.fromhex("0x1.fffffep127"), float.fromhex("0x1.ffffffp127"), 1e39, 1e300]
+    for s in (PT.SWITCH_NONE, max(0, L - 1)):
+        part = PT.build_partition(tr, eta, s)
+        nb = len(part)
+        sh = d * (L - part.level)
+        m = tr.leaf_start[(part.tgt + 1) << sh] - tr.leaf_start[part.tgt << sh]
+        n = tr.leaf_start[(part.src + 1) << sh] - tr.leaf_start[part.src << sh]
+        rank = np.minimum(rng.integers(0, 24, nb), np.minimum(m, n))
+        tot = np.exp(rng.uniform(-30, 5, nb))
+        nb2 = tot * (1 - rng.uniform(0, 1e-6, nb))
+        maxabs = np.exp(rng.uniform(-5, 12, nb))
+        hit = rng.random(nb) < 0.15
+        maxabs[hit] = rng.choice(edges, int(hit.sum()))
+        for pset in (W_MIXED, W_MIXED | (1 << 17), 1 | 4, 1 | 8, 1 | 2 | 8, 1 | 4 | 8 | (1 << 17), 1):
+            # hh_build compresses every block except leaf diagonals (and leaf neighbours when uniform)
+            dense0 = (part.kind == PT.DIAG) | ((part.kind == PT.LNBR) & ((pset & 15) == 1))
+            rk = np.where(dense0, 0, rank)
+            for eps in (1e-2, 1e-6):
+                ref = HM.tag_blocks(d, part.level, part.kind, m, n, rk, nb2, tot, maxabs, eps, pset)
+                got = hh.selftest_tags(tr.leaf_start, d, L, part.level, part.kind, part.tgt, part.src, rk,
+                                       nb2, tot, maxabs, eps, pset)
+                tagm = ref["storage"] == 0
+                np.testing.assert_array_equal(got["storage"], ref["storage"], err_msg=f"storage s={s} pset={pset}")
+                np.testing.assert_array_equal(got["rank"], ref["rank"], err_msg="rank")
+                np.testing.assert_array_equal(got["tag"][tagm], ref["tag"][tagm], err_msg=f"tag s={s} pset={pset}")
+                assert got["norm2"] == ref["norm2"]
+                assert (got["n_fallback"], got["n_promoted"]) == (ref["fallback"], ref["promoted"]), (pset, eps)
+                if pset == W_MIXED and eps == 1e-2:
+                    assert ref["promoted"] > 0 and len(set(ref["tag"][tagm])) >= 3
+
+
+W_MIXED = 15

@@ -71,6 +71,8 @@ def test_list_sizes_eta_sqrt2_2d():
     part = PT.build_partition(tr, np.sqrt(2.0), PT.SWITCH_NONE)
     assert _max_counts(part, [PT.FAR]) == 27
     assert _max_counts(part, [PT.LNBR]) == 8
+    c = PT.sparsity_constants(part, PT.SWITCH_NONE, tr.L)          # the function the bounds use
+    assert (c["c1"], c["c2"]) == (27, 8)
 
 
 def test_list_sizes_eta_sqrt3_3d():
@@ -81,6 +83,8 @@ def test_list_sizes_eta_sqrt3_3d():
     assert _max_counts(part, [PT.LNBR]) == 26
     hod = PT.build_partition(tr, np.sqrt(3.0), 0)
     assert _max_counts(hod, [PT.SIB]) == 7      # Eq. 2.7: C''' = 2^d - 1
+    assert PT.sparsity_constants(part, PT.SWITCH_NONE, tr.L)["c1"] == 189
+    assert PT.sparsity_constants(hod, 0, tr.L)["c3"] == 7
 
 
 def test_C_formulas_at_eta_sqrt_d():
