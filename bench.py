@@ -157,7 +157,7 @@ def oracle_sample(cfg: dict, target_bytes: float, seed: int = 0):
     w = np.where(dense, m * n, 16 * (m + n)).astype(float)
     w[np.maximum(m, n) > 2048] = 0.0
     order = rng.choice(len(part), size=min(len(part), 20000), replace=False, p=w / w.sum())
-    blocks, nbytes, picked = [], 0, 0
+    blocks, nbytes, picked, nstream = [], 0, 0, 0
     t_setup = time.perf_counter()
     for b in order:
         if nbytes >= target_bytes or time.perf_counter() - t_setup > 90:
@@ -169,19 +169,21 @@ def oracle_sample(cfg: dict, target_bytes: float, seed: int = 0):
         if part.kind[b] in (OP.DIAG,) or (part.kind[b] == OP.LNBR):
             blocks.append((i0, i1, j0, j1, "dense", A))
             nbytes += A.size * 8
+            nstream += A.size * 8
         else:
             c = OC.lr_compress(A, cfg["eps"])
             blocks.append((i0, i1, j0, j1, "lr", (c["U"].astype(np.float32).astype(np.float64),
                                                   c["W"].astype(np.float32).astype(np.float64))))
             nbytes += c["p"] * (A.shape[0] + A.shape[1]) * 4
+            nstream += c["p"] * (A.shape[0] + A.shape[1]) * 8
         picked += 1
-    return tr, blocks, nbytes
+    return tr, blocks, nbytes, nstream
 
 
 def oracle_rate(cfg: dict, seconds: float, steps: int | None = None):
     """Time the oracle's Alg. 3 (oracle.matvec.matvec_blocks, as it stands) over the sample."""
     from oracle import matvec as OM
-    tr, blocks, nbytes = oracle_sample(cfg, target_bytes=float(os.environ.get("HH_ORACLE_SAMPLE_BYTES", 1.5e8)))
+    tr, blocks, nbytes, nstream = oracle_sample(cfg, target_bytes=float(os.environ.get("HH_ORACLE_SAMPLE_BYTES", 1.5e8)))
     x = W.make_rhs(cfg, 1)
     times = []
     t_end = time.perf_counter() + seconds
@@ -196,7 +198,7 @@ def oracle_rate(cfg: dict, seconds: float, steps: int | None = None):
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
-    return nbytes, times, cores, len(blocks)
+    return nbytes, times, cores, len(blocks), nstream
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -226,6 +228,119 @@ def fp64_peaks():
         return {}
 
 
+def time_product(H, hh, cfg, nrhs, steps, warmup, flush_buf, dev, world, e2e_on=True):
+    """Device-timed hh_matvec steps (CUDA events on the launching stream, max over ranks), the
+    library's per-phase events, the launch count, and the e2e number through hh_matvec_host
+    (pinned host x / y, H2D + matvec + D2H inside the timed region)."""
+    import ctypes as C
+    import torch
+    x_h = W.make_rhs(cfg, nrhs)
+    x = torch.from_numpy(x_h.T.copy()).to(dev).T          # column-major (N, nrhs)
+    y = torch.empty_like(x.T).T
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        hh.hh_matvec(H, x, y, nrhs)
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.barrier()
+    hh.hh_matvec_timing(H)                        # reset
+    hh.hh_matvec_profile(H, True)
+    launches0 = hh.kernel_launches()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    for k in range(steps):
+        if flush_buf is not None:
+            flush_buf.fill_(float(k))
+        evs[k][0].record(stream)
+        hh.hh_matvec(H, x, y, nrhs)
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    launches = hh.kernel_launches() - launches0
+    hh.hh_matvec_profile(H, False)
+    phase_ms, nchunks = hh.hh_matvec_timing(H)
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs), dev)
+    e2e_ms = None
+    if e2e_on:
+        xp = torch.from_numpy(x_h.T.copy()).pin_memory()
+        yp = torch.empty_like(xp).pin_memory()
+        for _ in range(2):
+            hh.lib.hh_matvec_host(H.ptr, C.c_void_p(xp.data_ptr()), C.c_void_p(yp.data_ptr()), nrhs,
+                                  C.c_void_p(stream.cuda_stream))
+        ee = []
+        for k in range(max(3, steps // 2)):
+            if flush_buf is not None:
+                flush_buf.fill_(float(k))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st = hh.lib.hh_matvec_host(H.ptr, C.c_void_p(xp.data_ptr()), C.c_void_p(yp.data_ptr()), nrhs,
+                                       C.c_void_p(stream.cuda_stream))
+            b.record(stream)
+            assert st == 0
+            torch.cuda.synchronize()
+            ee.append(a.elapsed_time(b))
+        e2e_ms = max_over_ranks(sum(ee) / len(ee), dev)
+    # per-step phase times (the chunks of one step are summed: phase_ms covers steps x chunks)
+    per_step_chunks = max(1, nchunks // max(1, steps))
+    return dict(ms=ms, phase_ms=[v / max(1, steps) for v in phase_ms], nchunks=per_step_chunks,
+                launches=int(launches), e2e_ms=e2e_ms)
+
+
+def roofline(nrhs, split, phase_ms, config):
+    """Roofline of the dominant kernel (phase 1 streams W, phase 2 streams U + dense).  nrhs=1:
+    HBM-bound (2 flops per stored element); the multi-RHS contraction is compute-bound when
+    2 * nrhs flops per element exceed the ridge (FP64 peak / HBM peak): NR = 8, 16 run on the
+    FP64 tensor cores (DMMA), NR = 2, 4 on the FP64 FMA pipe (DFMA); FP64 peaks measured by
+    scripts/fp64_peak.cu (profiles/fp64_peak.json), the HBM peak is MEASURED_PEAKS.json."""
+    w_bytes, u_bytes, d_bytes, w_elems, u_elems = split
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs")
+    peak, peak_src = (hbm, "measured (MEASURED_PEAKS.json hbm_gbs)") if hbm else (6650.0, "fallback (B200_PROFILING.md)")
+    p1_ms, p2_ms = phase_ms[1], phase_ms[2]
+    kernels = {"phase1": (w_bytes, w_elems, p1_ms), "phase2": (u_bytes + d_bytes, u_elems, p2_ms)}
+    dom = max(kernels, key=lambda k: kernels[k][2])
+    alg_bytes, alg_elems, kms = kernels[dom]
+    fp = fp64_peaks()
+    mma = nrhs >= 8
+    fpeak = fp.get("dmma_tflops" if mma else "dfma_tflops")
+    flops = 2.0 * min(nrhs, 16) * alg_elems
+    compute_bound = fpeak is not None and flops / max(1, alg_bytes) > fpeak * 1e3 / peak
+    traffic, traffic_src = None, None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        key = config if nrhs == 1 else f"{config}_nrhs{nrhs}"
+        traffic = tj.get(key, {}).get(dom)
+        if traffic is not None:
+            traffic_src = (f"copied from profiles/ncu_traffic.json[{key}] (dram__bytes_read.sum + "
+                           f"dram__bytes_write.sum of one ncu --set full capture of this command: "
+                           f"{tj.get(key, {}).get('source', 'see profiles/README.md')}); not measured in this run")
+    except Exception:
+        pass
+    if compute_bound:
+        achieved = flops / (kms / 1e3) / 1e12 if kms > 0 else 0.0
+        roof = {"bound": "tensor" if mma else "alu", "kernel": f"k_phase{dom[-1]}", "achieved": round(achieved, 2),
+                "peak": fpeak, "peak_source": "measured FP64 " + ("DMMA" if mma else "DFMA") +
+                " (profiles/fp64_peak.json, scripts/fp64_peak.cu)", "unit": "TFLOP/s",
+                "frac": round(achieved / fpeak, 4), "traffic": traffic, "algorithmic_flops_per_launch": flops,
+                "algorithmic_bytes_per_launch": alg_bytes}
+    else:
+        achieved = alg_bytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+        roof = {"bound": "hbm", "kernel": f"k_phase{dom[-1]}", "achieved": round(achieved, 1), "peak": peak,
+                "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": alg_bytes}
+    roof["traffic_source"] = traffic_src
+    roof.update({"phase_ms_per_step": {"gather": round(phase_ms[0], 4), "phase1": round(p1_ms, 4),
+                                       "phase2": round(p2_ms, 4)},
+                 "phase1_GBps": round(w_bytes / (p1_ms / 1e3) / 1e9, 1) if p1_ms else None,
+                 "phase2_GBps": round((u_bytes + d_bytes) / (p2_ms / 1e3) / 1e9, 1) if p2_ms else None})
+    if nrhs > 1:
+        roof["phase1_TFLOPs"] = round(2.0 * min(nrhs, 16) * w_elems / (p1_ms / 1e3) / 1e12, 2) if p1_ms else None
+        roof["phase2_TFLOPs"] = round(2.0 * min(nrhs, 16) * u_elems / (p2_ms / 1e3) / 1e12, 2) if p2_ms else None
+    return roof
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     from paper_2604_09147_b200 import hh
@@ -245,113 +360,48 @@ def run_ours(args, rank, world, local_rank):
     del P
     info = hh.hh_info(H)
     ex = hh.hh_export(H, tables=True, arenas=False)
-    w_bytes, u_bytes, d_bytes, w_elems, u_elems = stored_split(ex)
+    split = stored_split(ex)
     del ex
     stored = info["stored_bytes"]
-    x_h = W.make_rhs(cfg, nrhs)
-    x = torch.from_numpy(x_h.T.copy()).to(dev).T          # column-major (N, nrhs)
-    y = torch.empty_like(x.T).T
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = stored < 4 * l2
     fbuf = torch.empty(int(2 * l2 // 4) + 1, dtype=torch.float32, device=dev) if flush else None
-    stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        hh.hh_matvec(H, x, y, nrhs)
-    torch.cuda.synchronize()
-    dist = world > 1
-    if dist:
-        import torch.distributed as tdist
-        tdist.barrier()
     clk = ClockSampler(local_rank)
     clk.start()
     time.sleep(0.3)
-    hh.hh_matvec_timing(H)                        # reset
-    hh.hh_matvec_profile(H, True)
-    launches0 = hh.kernel_launches()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    torch.cuda.synchronize()
-    if dist:
-        tdist.barrier()
-    t_wall = time.perf_counter()
-    for k in range(args.steps):
-        if flush:
-            fbuf.fill_(float(k))
-        evs[k][0].record(stream)
-        hh.hh_matvec(H, x, y, nrhs)
-        evs[k][1].record(stream)
-    torch.cuda.synchronize()
-    t_wall = time.perf_counter() - t_wall
-    launches = hh.kernel_launches() - launches0
-    hh.hh_matvec_profile(H, False)
-    phase_ms, nchunks = hh.hh_matvec_timing(H)
+    r = time_product(H, hh, cfg, nrhs, args.steps, args.warmup, fbuf, dev, world, not args.no_e2e)
+    multi = None
+    if args.multi_rhs and nrhs == 1:
+        # BASELINE config 3 is "nrhs=1 and nrhs=16": the 16-RHS product on the same resident
+        # H-hat, same box and run, its own roofline (FP64 tensor cores) and e2e
+        nm = 16
+        rm = time_product(H, hh, cfg, nm, args.steps, args.warmup, fbuf, dev, world, not args.no_e2e)
+        rm_step = rm["ms"] / args.steps
+        multi = {"nrhs": nm, "value": round(job_gbps(stored, args.steps, world, rm["ms"]), 2), "unit": "GB/s",
+                 "ms_per_step": round(rm_step, 4),
+                 "rhs_columns_per_s": round(world * args.steps * nm / (rm["ms"] / 1e3), 2),
+                 "matvecs_per_s": round(world * args.steps / (rm["ms"] / 1e3), 3),
+                 "speedup_vs_16_single_rhs": round(16 * (r["ms"] / args.steps) / rm_step, 3),
+                 "roofline": roofline(nm, split, rm["phase_ms"], args.config),
+                 "gpu_launches": rm["launches"]}
+        if rm["e2e_ms"] is not None:
+            multi["e2e"] = {"value": round(stored * world / (rm["e2e_ms"] / 1e3) / 1e9, 2), "unit": "GB/s",
+                            "rhs_columns_per_s": round(world * nm * 1e3 / rm["e2e_ms"], 2),
+                            "ms_per_step": round(rm["e2e_ms"], 4),
+                            "h2d_bytes_per_step": int(8 * cfg["N"] * nm), "d2h_bytes_per_step": int(8 * cfg["N"] * nm)}
     clocks = clk.stop()
-    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs), dev)
+    ms = r["ms"]
     per_step = ms / args.steps
     value = job_gbps(stored, args.steps, world, ms)
-    # e2e: host buffers through hh_matvec_host (H2D of x, matvec, D2H of y inside)
     e2e = None
-    if not args.no_e2e:
-        xp = torch.from_numpy(x_h.T.copy()).pin_memory()
-        yp = torch.empty_like(xp).pin_memory()
-        import ctypes as C
-        for _ in range(2):
-            hh.lib.hh_matvec_host(H.ptr, C.c_void_p(xp.data_ptr()), C.c_void_p(yp.data_ptr()), nrhs,
-                                  C.c_void_p(stream.cuda_stream))
-        ee = []
-        for k in range(max(3, args.steps // 2)):
-            if flush:
-                fbuf.fill_(float(k))
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            st = hh.lib.hh_matvec_host(H.ptr, C.c_void_p(xp.data_ptr()), C.c_void_p(yp.data_ptr()), nrhs,
-                                       C.c_void_p(stream.cuda_stream))
-            b.record(stream)
-            assert st == 0
-            torch.cuda.synchronize()
-            ee.append(a.elapsed_time(b))
-        e_ms = max_over_ranks(sum(ee) / len(ee), dev)
+    if r["e2e_ms"] is not None:
+        e_ms = r["e2e_ms"]
         e2e = {"value": round(stored * world / (e_ms / 1e3) / 1e9, 2), "unit": "GB/s",
                "matvecs_per_s": round(world * 1e3 / e_ms, 3), "ms_per_step": round(e_ms, 4),
                "h2d_bytes_per_step": int(8 * cfg["N"] * nrhs), "d2h_bytes_per_step": int(8 * cfg["N"] * nrhs)}
-    # roofline of the dominant kernel (phase 1 streams W, phase 2 streams U + dense)
     peaks = measured_peaks()
-    hbm = peaks.get("hbm_gbs")
-    peak, peak_src = (hbm, "measured (MEASURED_PEAKS.json hbm_gbs)") if hbm else (6650.0, "fallback (B200_PROFILING.md)")
-    p1_ms = phase_ms[1] / max(1, nchunks)
-    p2_ms = phase_ms[2] / max(1, nchunks)
-    kernels = {"phase1": (w_bytes, w_elems, p1_ms), "phase2": (u_bytes + d_bytes, u_elems, p2_ms)}
-    dom = max(kernels, key=lambda k: kernels[k][2])
-    alg_bytes, alg_elems, kms = kernels[dom]
-    # roofline: 2 * nrhs flops per stored element; the kernel is compute-bound when that
-    # intensity exceeds the ridge (FP64 peak / HBM peak).  NR = 8, 16 run on the FP64 tensor
-    # cores (DMMA), NR = 2, 4 on the FP64 FMA pipe (DFMA); peaks measured by scripts/fp64_peak.cu.
-    fp = fp64_peaks()
-    mma = nrhs >= 8
-    fpeak = fp.get("dmma_tflops" if mma else "dfma_tflops")
-    flops = 2.0 * min(nrhs, 16) * alg_elems
-    compute_bound = fpeak is not None and flops / max(1, alg_bytes) > fpeak * 1e3 / peak
-    traffic = None
-    try:
-        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tj.get(args.config if nrhs == 1 else f"{args.config}_nrhs{nrhs}", {}).get(dom)
-    except Exception:
-        pass
-    if compute_bound:
-        achieved = flops / (kms / 1e3) / 1e12 if kms > 0 else 0.0
-        roof = {"bound": "tensor" if mma else "alu", "kernel": f"k_phase{dom[-1]}", "achieved": round(achieved, 2),
-                "peak": fpeak, "peak_source": "measured FP64 " + ("DMMA" if mma else "DFMA") +
-                " (profiles/fp64_peak.json, scripts/fp64_peak.cu)", "unit": "TFLOP/s",
-                "frac": round(achieved / fpeak, 4), "traffic": traffic, "algorithmic_flops_per_launch": flops,
-                "algorithmic_bytes_per_launch": alg_bytes}
-    else:
-        achieved = alg_bytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
-        roof = {"bound": "hbm", "kernel": f"k_phase{dom[-1]}", "achieved": round(achieved, 1), "peak": peak,
-                "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "algorithmic_bytes_per_launch": alg_bytes}
-    roof.update({"phase_ms_per_step": {"gather": round(phase_ms[0] / max(1, nchunks), 4), "phase1": round(p1_ms, 4),
-                                       "phase2": round(p2_ms, 4)},
-                 "phase1_GBps": round(w_bytes / (p1_ms / 1e3) / 1e9, 1) if p1_ms else None,
-                 "phase2_GBps": round((u_bytes + d_bytes) / (p2_ms / 1e3) / 1e9, 1) if p2_ms else None})
+    peak = peaks.get("hbm_gbs") or 6650.0
+    roof = roofline(nrhs, split, r["phase_ms"], args.config)
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(per_step, 4), "higher_is_better": True, "scaling": "weak",
@@ -365,22 +415,30 @@ def run_ours(args, rank, world, local_rank):
                    "stored_bytes_by_tag": dict(zip(["fp64", "fp32", "fp16", "bf16", "dense_fp64"], info["stored_bytes_tag"])),
                    "nblocks": info["nblocks"], "total_rank": info["total_rank"], "L": info["L"],
                    "l2_policy": "flush (2x L2 write) before each step" if flush else "inputs larger than L2",
-                   "build_seconds": round(build_s, 2)},
+                   "build_seconds": round(build_s, 2), "n_inexact": info.get("n_inexact"),
+                   "n_promoted": info["n_promoted"]},
         "frac_of_hbm_peak": round(value / world / peak, 4),
         "roofline": roof,
         "e2e": e2e,
+        "multi_rhs": multi,
         "storage_ratio": storage_ratio("sweep" if args.config == "sweep" else args.config, stored),
         "paper_context": PAPER_CONTEXT,
-        "gpu_launches": int(launches),
+        "gpu_launches": r["launches"],
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        nbytes, times, cores, nblk = oracle_rate(cfg, seconds=args.cpu_seconds)
+        nbytes, times, cores, nblk, nstream = oracle_rate(cfg, seconds=args.cpu_seconds)
         med = statistics.median(times)
         line["cpu_baseline"] = {"value": round(nbytes / med / 1e9, 4), "unit": "GB/s", "cores": cores,
                                 "kind": "oracle",
-                                "sample": f"{nblk} blocks of {args.config} ({nbytes / 1e6:.1f} MB stored), oracle "
-                                          f"Alg. 3 (oracle/matvec.py) x{len(times)} passes, median",
+                                "sample": f"{nblk} blocks of {args.config} ({nbytes / 1e6:.1f} MB stored at the "
+                                          f"workload's storage widths: low-rank counted at fp32, 4 B/element, the "
+                                          f"tag of 92% of its low-rank bytes; dense fp64), oracle Alg. 3 "
+                                          f"(oracle/matvec.py, numpy fp64 arrays as it stands) x{len(times)} "
+                                          f"passes, median",
+                                "bytes_streamed_GBps": round(nstream / med / 1e9, 4),
+                                "bytes_streamed_note": "the oracle holds every factor as fp64 (8 B/element): "
+                                                       f"{nstream / 1e6:.1f} MB read per pass",
                                 "matvecs_per_s_equiv": round(nbytes / med / stored, 6)}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -395,7 +453,7 @@ def run_reference(args, rank, world):
     # against the GPU build's stored bytes recorded in profiles/ (if present)
     for _ in range(args.warmup):
         pass
-    nbytes, times, cores, nblk = oracle_rate(cfg, seconds=0.0, steps=args.warmup + args.steps)
+    nbytes, times, cores, nblk, nstream = oracle_rate(cfg, seconds=0.0, steps=args.warmup + args.steps)
     times = times[args.warmup:]
     tot = sum(times)
     value = nbytes * len(times) / tot / 1e9
@@ -423,6 +481,8 @@ def main():
     ap.add_argument("--pset", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-multi-rhs", dest="multi_rhs", action="store_false",
+                    help="skip the 16-RHS sub-record (default: on for nrhs=1)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

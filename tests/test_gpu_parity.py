@@ -44,7 +44,6 @@ def test_check1b_ranks_and_tags(built):
     bad_r, bad_t, st = PL.rank_tag_parity(ex, Ho)
     print(name, st)
     assert bad_r == 0 and bad_t == 0, st
-    assert st["rank_diff"] <= max(1, st["n_lr"] // 1000), st
     # ||H~||^2 agrees with the oracle's Alg. 4 value
     assert abs(ex["info"]["norm2"] - Ho.norm2) <= 1e-12 * Ho.norm2
 
@@ -104,21 +103,27 @@ def test_global_error_thm42(built):
 
 
 def test_determinism_bitwise(built):
-    """No atomics in the arithmetic, fixed summation orders: bitwise-identical y across runs,
-    across streams and for the same column inside different nrhs chunks' widths."""
+    """No atomics in the arithmetic, fixed summation orders: bitwise-identical y across runs and
+    across streams, for every RHS-chunk kernel width (2: DFMA; 16: DMMA with the phase-2
+    leaf-end reduction in the leaf's last TMA stage; 20: a 16-wide then a 4-wide chunk).  A
+    column's bits depend on its chunk width (different contraction kernels), not on the run."""
     _, cfg, P, H, ex, Ho = built
-    x = W.make_rhs(cfg, 2)
-    y1 = PL.gpu_matvec(H, x)
-    y2 = PL.gpu_matvec(H, x)
-    assert np.array_equal(y1, y2)
-    s = torch.cuda.Stream()
-    xd = torch.from_numpy(x.T.copy()).cuda().T
-    yd = torch.empty_like(xd.T).T
-    torch.cuda.synchronize()
-    with torch.cuda.stream(s):
-        hh.hh_matvec(H, xd, yd, 2, stream=s)
-    s.synchronize()
-    assert np.array_equal(yd.cpu().numpy(), y1)
+    for nrhs in (2, 16, 20):
+        x = W.make_rhs(cfg, nrhs)
+        y1 = PL.gpu_matvec(H, x)
+        y2 = PL.gpu_matvec(H, x)
+        assert np.array_equal(y1, y2), nrhs
+        s = torch.cuda.Stream()
+        xd = torch.from_numpy(x.T.copy()).cuda().T
+        yd = torch.empty_like(xd.T).T
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s):
+            hh.hh_matvec(H, xd, yd, nrhs, stream=s)
+        s.synchronize()
+        assert np.array_equal(yd.cpu().numpy(), y1), nrhs
+    # the first 16 columns of the 20-column product are the 16-column product's columns
+    x = W.make_rhs(cfg, 20)
+    assert np.array_equal(PL.gpu_matvec(H, x)[:, :16], PL.gpu_matvec(H, np.asfortranarray(x[:, :16])))
 
 
 def test_rounding_routines_match_oracle():
@@ -312,3 +317,47 @@ def test_host_buffer_entry_point_matches_device_path():
         yd = PL.gpu_matvec(H, x)
         yh = hh.hh_matvec_host(H, np.asfortranarray(x))
         assert np.array_equal(np.asarray(yh).reshape(yd.shape, order="F"), yd)
+
+
+def test_beneficial_rule_parity_pure_hs_mixed():
+    """PAPER.md:992 on the device: mixed pure H_s (2D log, eps=1e-8, leaf 16) keeps some leaf
+    neighbours dense and compresses others; storage kind, rank and tag of every block equal the
+    oracle's (no unexplained storage difference), and the matvec matches on the exported data."""
+    P = W.points_uniform(1500, 2, 12)
+    cfg = dict(kernel=W.K_LOG, scale=1.0, eps=1e-8, eta=1.0, leaf=16, s=PT.SWITCH_NONE, pset=W.P_MIXED)
+    H = PL.gpu_build(P, cfg)
+    ex = PL.export(H)
+    Ho = PL.oracle_build(P, cfg)
+    PL.check_partition(ex, Ho)
+    bad_r, bad_t, st = PL.rank_tag_parity(ex, Ho)
+    assert bad_r == 0 and bad_t == 0, st
+    B = ex["blocks"]
+    ln = B["kind"] == PT.LNBR
+    assert np.sum(ln & (B["storage"] == 1)) > 100 and np.sum(ln & (B["storage"] == 0)) > 100, st
+    assert st["storage_diff"] == 0, st
+    lay = PL.check_packing(ex)
+    x = W.rhs(1500, 3, 4, "uniform_pm1")
+    assert PL.rel2(PL.gpu_matvec(H, x), PL.oracle_matvec_on_export(ex, lay, x)) <= 1e-12
+
+
+@pytest.mark.parametrize("scale,kernel,pset", [(1e-20, W.K_INV_R2, W.P_MIXED),
+                                               (1e-3, W.K_INV_R, W.P_FP64 | W.P_FP32 | W.P_FP16),
+                                               (1e-3, W.K_INV_R, W.P_FP64 | W.P_FP16)])
+def test_range_guard_promotion_parity(scale, kernel, pset):
+    """Range guard (reading G16): on domains small enough that factor entries overflow the
+    16/32-bit formats (1/r^2 ~ 1e40 on 1e-20; 1/r ~ 1e5 on 1e-3), blocks are promoted to the
+    next smaller u in the set; the promoted count, every tag and the matvec equal the oracle's."""
+    P = W.points_uniform(600, 2, 5) * scale
+    cfg = dict(kernel=kernel, scale=1.0, eps=1e-2, eta=1.0, leaf=16, s=2, pset=pset)
+    H = PL.gpu_build(P, cfg)
+    ex = PL.export(H)
+    Ho = PL.oracle_build(P, cfg)
+    PL.check_partition(ex, Ho)
+    bad_r, bad_t, st = PL.rank_tag_parity(ex, Ho)
+    assert bad_r == 0 and bad_t == 0, st
+    assert Ho.promoted > 0 and ex["info"]["n_promoted"] == Ho.promoted, (ex["info"]["n_promoted"], Ho.promoted)
+    lay = PL.check_packing(ex)
+    x = W.rhs(600, 2, 6, "uniform_pm1")
+    y = PL.gpu_matvec(H, x)
+    assert np.all(np.isfinite(y))
+    assert PL.rel2(y, PL.oracle_matvec_on_export(ex, lay, x)) <= 1e-12
