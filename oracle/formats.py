@@ -1,8 +1,14 @@
 """Floating-point storage formats of Table 1 and round-to-nearest-even (oracle).
 
-PAPER.md:37-50 (Table 1) lists fp64, fp32, fp16, bf16 (and q43, excluded by BASELINE).
+PAPER.md:37-50 (Table 1) lists fp64, fp32, fp16, bf16 and the 8-bit q43 (1-4-3, e_min -6,
+e_max 7, x_max 240).  BASELINE's precision set is {fp64, fp32, fp16, bf16}; q43 is the NEXT-3
+opt-in (precision_set bit 16).
 Reading G12: the unit roundoffs are the exact powers of two
-u = 2^-(m+1): 2^-53, 2^-24, 2^-11, 2^-8 (Table 1 prints them rounded).
+u = 2^-(m+1): 2^-53, 2^-24, 2^-11, 2^-8, 2^-4 (Table 1 prints them rounded; its q43 entry
+2.5e-1 is garbled — 2^-(3+1) = 6.25e-2).  q43 is the IEEE-style 8-bit format of Table 1:
+exponent field 15 is inf/NaN, so x_max = (2 - 2^-3) 2^7 = 240 and the smallest subnormal is
+2^-9; its encodings of |x| <= 240 coincide with the OCP FP8 E4M3 ones (which reuse exponent
+15 for 256..448), so the device decodes them with the E4M3 rules.
 Reading G16: storage rounding is a SINGLE round-to-nearest-even from float64 directly
 to the target format, subnormals kept, overflow -> +-inf (the range guard in hmatrix.py
 then promotes the block, so no inf is ever stored).
@@ -16,10 +22,11 @@ from __future__ import annotations
 
 import numpy as np
 
-FP64, FP32, FP16, BF16 = 0, 1, 2, 3          # tag ids (same numbering as include/hh.h)
-TAG_NAMES = {FP64: "fp64", FP32: "fp32", FP16: "fp16", BF16: "bf16"}
-TAG_BIT = {FP64: 1, FP32: 2, FP16: 4, BF16: 8}  # precision_set bitmask
-BYTES = {FP64: 8, FP32: 4, FP16: 2, BF16: 2}
+FP64, FP32, FP16, BF16, Q43 = 0, 1, 2, 3, 4    # tag ids (same numbering as include/hh.h)
+TAGS = (FP64, FP32, FP16, BF16, Q43)
+TAG_NAMES = {FP64: "fp64", FP32: "fp32", FP16: "fp16", BF16: "bf16", Q43: "q43"}
+TAG_BIT = {FP64: 1, FP32: 2, FP16: 4, BF16: 8, Q43: 16}  # precision_set bitmask
+BYTES = {FP64: 8, FP32: 4, FP16: 2, BF16: 2, Q43: 1}
 BITS = {t: 8 * b for t, b in BYTES.items()}
 
 # (mantissa bits m, e_min, e_max) — Table 1 columns (1-e-m), e_min, e_max
@@ -28,6 +35,7 @@ PARAMS = {
     FP32: (23, -126, 127),
     FP16: (10, -14, 15),
     BF16: (7, -126, 127),
+    Q43: (3, -6, 7),
 }
 
 
@@ -84,8 +92,23 @@ def to_storage_bits(x64, tag: int) -> np.ndarray:
         return r.astype(np.float32).view(np.uint32)
     if tag == FP16:
         return r.astype(np.float16).view(np.uint16)
-    f32 = r.astype(np.float32).view(np.uint32)
-    return (f32 >> np.uint32(16)).astype(np.uint16)
+    if tag == BF16:
+        f32 = r.astype(np.float32).view(np.uint32)
+        return (f32 >> np.uint32(16)).astype(np.uint16)
+    # q43 (1-4-3, bias 7): sign | exponent field | 3 mantissa bits, from the exact rounded value
+    a = np.abs(r)
+    sign = (np.signbit(r)).astype(np.uint8) << np.uint8(7)
+    out = np.zeros(a.shape, np.uint8)
+    inf = np.isinf(a)
+    norm = (a >= 2.0 ** -6) & ~inf
+    _, e = np.frexp(a[norm])                      # a = f 2^e, f in [0.5, 1)
+    E = e.astype(np.int64) - 1
+    mant = np.ldexp(a[norm], -E) * 8 - 8          # exact: a has at most 4 significant bits
+    out[norm] = ((E + 7) << 3 | mant.astype(np.int64)).astype(np.uint8)
+    sub = (a < 2.0 ** -6) & ~inf
+    out[sub] = np.ldexp(a[sub], 9).astype(np.int64).astype(np.uint8)   # a = m 2^-9, m < 8
+    out[inf] = 0x78
+    return out | sign
 
 
 def from_storage_bytes(buf: bytes | np.ndarray, tag: int) -> np.ndarray:
@@ -97,5 +120,12 @@ def from_storage_bytes(buf: bytes | np.ndarray, tag: int) -> np.ndarray:
         return b.view("<f4").astype(np.float64)
     if tag == FP16:
         return b.view("<f2").astype(np.float64)
-    hi = b.view("<u2").astype(np.uint32) << np.uint32(16)
-    return hi.view(np.float32).astype(np.float64)
+    if tag == BF16:
+        hi = b.view("<u2").astype(np.uint32) << np.uint32(16)
+        return hi.view(np.float32).astype(np.float64)
+    # q43: (-1)^s (1 + m/8) 2^(e-7) for exponent field e in 1..14, (-1)^s (m/8) 2^-6 for e = 0
+    e = ((b >> 3) & 0xF).astype(np.int64)
+    m = (b & 0x7).astype(np.float64)
+    v = np.where(e == 0, np.ldexp(m / 8.0, -6), np.ldexp(1.0 + m / 8.0, e - 7))
+    v = np.where(e == 15, np.inf, v)
+    return np.where(b & 0x80, -v, v)

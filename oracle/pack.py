@@ -70,8 +70,8 @@ def pack(leaf_start, d, L, level, tgt, src, rank, tag, storage):
     w_off = np.full(nb, -1, np.int64)
     wcol = np.full(nb, -1, np.int64)
     wpanel = np.full(nb, -1, np.int64)
-    w_bytes = np.zeros(4, np.int64)
-    for g in range(4):
+    w_bytes = np.zeros(len(F.TAGS), np.int64)
+    for g in F.TAGS:
         idx = np.nonzero(lr & (tag == g) & (rank > 0))[0]
         order = idx[np.lexsort((tgt[idx], src[idx], level[idx]))]
         off = 0
@@ -93,13 +93,13 @@ def pack(leaf_start, d, L, level, tgt, src, rank, tag, storage):
 
     # U arenas: per-group column totals G[l][(t, g)], ucol per block
     ucol = np.full(nb, -1, np.int64)
-    leaf_cols = np.zeros((4, ncell), np.int64)
+    leaf_cols = np.zeros((len(F.TAGS), ncell), np.int64)
     leaf_ids = np.arange(ncell, dtype=np.int64)
     for l in range(0, L + 1):
         sel = np.nonzero(lr & (level == l) & (rank > 0))[0]
         if sel.size == 0:
             continue
-        for g in range(4):
+        for g in F.TAGS:
             sg = sel[tag[sel] == g]
             if sg.size == 0:
                 continue
@@ -119,8 +119,8 @@ def pack(leaf_start, d, L, level, tgt, src, rank, tag, storage):
             ucol[o] = leaf_cols[g, anc_leaf] + within
             leaf_cols[g] += tot_t[leaf_ids >> (d * (L - l))]
     nR = np.diff(leaf_start)
-    u_leaf_off = np.zeros((4, ncell + 1), np.int64)
-    for g in range(4):
+    u_leaf_off = np.zeros((len(F.TAGS), ncell + 1), np.int64)
+    for g in F.TAGS:
         sz = align_up(nR * leaf_cols[g] * F.BYTES[g])
         u_leaf_off[g, 1:] = np.cumsum(sz)
 

@@ -26,7 +26,10 @@ hh_status fail(hh_status s, const std::string &m) {
 __global__ void k_round(const double *in, int64_t n, int tag, uint32_t *out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  out[i] = tag == TAG_FP32 ? to_fp32_bits(in[i]) : tag == TAG_FP16 ? to_fp16_bits(in[i]) : to_bf16_bits(in[i]);
+  out[i] = tag == TAG_FP32   ? to_fp32_bits(in[i])
+           : tag == TAG_FP16 ? to_fp16_bits(in[i])
+           : tag == TAG_BF16 ? to_bf16_bits(in[i])
+                             : to_q43_bits(in[i]);
 }
 
 __global__ void k_leaf_of(const int64_t *leaf_start, int64_t ncell, int32_t *leaf_of) {
@@ -155,7 +158,7 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
   if (leaf_size < 1) return fail(HH_EINVAL, "leaf_size must be >= 1");
   if (leaf_size > 256) return fail(HH_EUNSUPPORTED, "leaf_size > 256 not supported by this build");
   if (!(precision_set & HH_P_FP64)) return fail(HH_EINVAL, "precision_set must contain HH_P_FP64");
-  if (precision_set & ~(0xFu | HH_LEDGER_ONLY | HH_TIE_FP16)) return fail(HH_EINVAL, "unknown precision_set bits");
+  if (precision_set & ~(0x1Fu | HH_LEDGER_ONLY | HH_TIE_FP16)) return fail(HH_EINVAL, "unknown precision_set bits");
   if (kernel.kind < 0 || kernel.kind > 4) return fail(HH_EINVAL, "unknown kernel kind");
   if ((kernel.kind == HH_K_GAUSS || kernel.kind == HH_K_EXP) && !(kernel.scale > 0.0))
     return fail(HH_EINVAL, "kernel scale must be > 0");
@@ -174,7 +177,7 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
     H->eta = eta;
     H->leaf_size = leaf_size;
     H->s = switch_level;
-    H->pset = precision_set & 0xF;
+    H->pset = precision_set & 0x1F;
     H->ledger = (precision_set & HH_LEDGER_ONLY) != 0;
     H->tie16 = (precision_set & HH_TIE_FP16) && (precision_set & HH_P_FP16) && (precision_set & HH_P_BF16);
     DBuf pts;
@@ -204,7 +207,7 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
     assign_tags(H);                                                   // a4 + a5
     compute_layout(H);                                                // a6 (offsets)
     if (!H->ledger) {
-      for (int g = 0; g < 4; ++g) {
+      for (int g = 0; g < NTAG; ++g) {
         H->W[g].alloc(H->w_bytes[g]);
         H->U[g].alloc(H->u_bytes[g]);
         HH_CUDA(cudaMemsetAsync(H->U[g].p, 0, H->U[g].bytes, st));
@@ -220,7 +223,7 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
       k_leaf_of<<<1184, 256, 0, st>>>(d_ls.as<int64_t>(), H->ncell, d_leaf_of.as<int32_t>());
       HH_LAUNCHED();
       Arenas ar{};
-      for (int g = 0; g < 4; ++g) {
+      for (int g = 0; g < NTAG; ++g) {
         ar.W[g] = H->W[g].as<uint8_t>();
         ar.U[g] = H->U[g].as<uint8_t>();
       }
@@ -282,7 +285,7 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
     I.nblocks = (int64_t)nb;
     I.total_rank = H->ztotal;
     I.norm2 = H->norm2;
-    for (int g = 0; g < 4; ++g) {
+    for (int g = 0; g < NTAG; ++g) {
       I.w_bytes[g] = H->w_bytes[g];
       I.u_bytes[g] = H->u_bytes[g];
     }
@@ -436,12 +439,13 @@ hh_status hh_export(hh_handle H, hh_export_t *out) {
     if (out->arena_dst && out->arena_len > 0) {
       if (H->ledger) return fail(HH_EINVAL, "ledger-only handle has no arenas");
       const DBuf *src = nullptr;
-      if (out->arena >= 0 && out->arena < 4) src = &H->W[out->arena];
-      else if (out->arena >= 4 && out->arena < 8) src = &H->U[out->arena - 4];
-      else if (out->arena == 8) src = &H->D;
-      if (!src) return fail(HH_EINVAL, "arena must be 0..8");
-      const int64_t size = out->arena < 4 ? H->w_bytes[out->arena]
-                           : out->arena < 8 ? H->u_bytes[out->arena - 4] : H->d_bytes;
+      if (out->arena >= 0 && out->arena < NTAG) src = &H->W[out->arena];
+      else if (out->arena >= NTAG && out->arena < 2 * NTAG) src = &H->U[out->arena - NTAG];
+      else if (out->arena == 2 * NTAG) src = &H->D;
+      if (!src) return fail(HH_EINVAL, "arena must be 0..10");
+      const int64_t size = out->arena < NTAG       ? H->w_bytes[out->arena]
+                           : out->arena < 2 * NTAG ? H->u_bytes[out->arena - NTAG]
+                                                   : H->d_bytes;
       if (out->arena_off < 0 || out->arena_off + out->arena_len > size) return fail(HH_EINVAL, "arena window out of range");
       HH_CUDA(cudaMemcpy(out->arena_dst, (const char *)src->p + out->arena_off, out->arena_len, cudaMemcpyDeviceToHost));
     }
@@ -462,7 +466,7 @@ hh_status hh_switch_level_search(const double *points, int64_t N, int32_t d, hh_
                                  int32_t *out_level, int32_t *out_L, int64_t *bytes, int32_t bytes_len) {
   g_err.clear();
   if (!out_level) return fail(HH_EINVAL, "NULL pointer");
-  const uint32_t pset = (precision_set & 0xFu) | HH_LEDGER_ONLY;
+  const uint32_t pset = (precision_set & (0x1Fu | HH_TIE_FP16)) | HH_LEDGER_ONLY;
   auto ledger_bytes = [&](int32_t s, int64_t &out, int32_t *L) -> hh_status {
     hh_handle h = nullptr;
     const hh_status st = hh_build(points, N, d, kernel, eps, eta, leaf_size, s, pset, cuda_stream, &h);
@@ -567,7 +571,7 @@ hh_status hh_selftest_layout(const int64_t *leaf_start, int32_t d, int32_t L, in
     if (u_leaf_off) std::copy(H.u_leaf_off.begin(), H.u_leaf_off.end(), u_leaf_off);
     if (d_leaf_off) std::copy(H.d_leaf_off.begin(), H.d_leaf_off.end(), d_leaf_off);
     if (w_bytes)
-      for (int g = 0; g < 4; ++g) w_bytes[g] = H.w_bytes[g];
+      for (int g = 0; g < NTAG; ++g) w_bytes[g] = H.w_bytes[g];
     return HH_OK;
   } catch (const Error &e) {
     return fail(e.st, e.what());
@@ -591,7 +595,7 @@ hh_status hh_selftest_tags(const int64_t *leaf_start, int32_t d, int32_t L, int6
     H.eps = eps;
     H.ncell = 1ll << (d * L);
     H.leaf_start.assign(leaf_start, leaf_start + H.ncell + 1);
-    H.pset = precision_set & 0xF;
+    H.pset = precision_set & 0x1F;
     H.tie16 = (precision_set & HH_TIE_FP16) && (precision_set & HH_P_FP16) && (precision_set & HH_P_BF16);
     H.level.assign(level, level + nblocks);
     H.kind.assign(kind, kind + nblocks);
@@ -627,7 +631,7 @@ hh_status hh_selftest_tags(const int64_t *leaf_start, int32_t d, int32_t L, int6
  * return the bit patterns (checked against the oracle's definition-based rounding). */
 hh_status hh_selftest_round(const double *host_in, int64_t n, int32_t tag, uint32_t *host_bits) {
   g_err.clear();
-  if (!host_in || !host_bits || n < 0 || tag < 1 || tag > 3) return fail(HH_EINVAL, "bad argument");
+  if (!host_in || !host_bits || n < 0 || tag < 1 || tag > 4) return fail(HH_EINVAL, "bad argument");
   try {
     DBuf a, b;
     a.alloc(sizeof(double) * n);

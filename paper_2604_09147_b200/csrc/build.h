@@ -21,9 +21,9 @@ struct CompressResult {
 
 // Pass-2 output placement (device pointers).
 struct Arenas {
-  uint8_t *W[4];
-  uint8_t *U[4];
-  const int64_t *u_leaf_off;  // [4][ncell+1]
+  uint8_t *W[NTAG];
+  uint8_t *U[NTAG];
+  const int64_t *u_leaf_off;  // [NTAG][ncell+1]
   const int64_t *leaf_start;  // [ncell+1]
   const int32_t *leaf_of;     // [N] tree position -> leaf cell
   int64_t ncell;

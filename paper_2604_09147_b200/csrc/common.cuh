@@ -46,11 +46,12 @@ void count_launch(int n = 1);  // launch accounting (api.cpp)
   } while (0)
 
 // ------------------------------------------------------------------ constants
-constexpr int TAG_FP64 = 0, TAG_FP32 = 1, TAG_FP16 = 2, TAG_BF16 = 3;
+constexpr int TAG_FP64 = 0, TAG_FP32 = 1, TAG_FP16 = 2, TAG_BF16 = 3, TAG_Q43 = 4;
+constexpr int NTAG = 5;
 constexpr int KIND_FAR = 0, KIND_NBR = 1, KIND_SIB = 2, KIND_LNBR = 3, KIND_DIAG = 4;
 constexpr int STORE_LR = 0, STORE_DENSE = 1;
 constexpr int64_t ALIGN = 16;
-__host__ __device__ inline int tag_bytes(int t) { return t == TAG_FP64 ? 8 : (t == TAG_FP32 ? 4 : 2); }
+__host__ __device__ inline int tag_bytes(int t) { return t == TAG_FP64 ? 8 : t == TAG_FP32 ? 4 : t == TAG_Q43 ? 1 : 2; }
 inline int64_t align_up(int64_t x, int64_t a = ALIGN) { return (x + a - 1) / a * a; }
 
 // ------------------------------------------------------------------ kernel functions
@@ -86,7 +87,7 @@ __host__ __device__ inline uint32_t rne_bits(double x) {
   memcpy(&b, &x, 8);
   const uint32_t sign = (uint32_t)(b >> 63);
   const uint64_t a = b & 0x7FFFFFFFFFFFFFFFull;
-  constexpr int EBITS = (EMAX == 15) ? 5 : 8;
+  constexpr int EBITS = (EMAX == 15) ? 5 : (EMAX == 7) ? 4 : 8;
   constexpr uint32_t INF = ((1u << EBITS) - 1u) << M;
   const uint32_t sbit = sign << (M + EBITS);
   if (a >= 0x7FF0000000000000ull) {  // inf / nan
@@ -128,5 +129,7 @@ __host__ __device__ inline uint32_t rne_bits(double x) {
 __host__ __device__ inline uint16_t to_fp16_bits(double x) { return (uint16_t)rne_bits<10, -14, 15>(x); }
 __host__ __device__ inline uint16_t to_bf16_bits(double x) { return (uint16_t)rne_bits<7, -126, 127>(x); }
 __host__ __device__ inline uint32_t to_fp32_bits(double x) { return rne_bits<23, -126, 127>(x); }
+// q43 (Table 1: 1-4-3, e_min -6, e_max 7): exponent field 15 = inf, x_max = 240
+__host__ __device__ inline uint8_t to_q43_bits(double x) { return (uint8_t)rne_bits<3, -6, 7>(x); }
 
 }  // namespace hh

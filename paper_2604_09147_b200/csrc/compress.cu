@@ -586,8 +586,11 @@ __device__ __forceinline__ void store_tagged(uint8_t *base, int64_t elem, int ta
     case TAG_FP16:
       reinterpret_cast<uint16_t *>(base)[elem] = to_fp16_bits(v);
       break;
-    default:
+    case TAG_BF16:
       reinterpret_cast<uint16_t *>(base)[elem] = to_bf16_bits(v);
+      break;
+    default:
+      base[elem] = to_q43_bits(v);
   }
 }
 

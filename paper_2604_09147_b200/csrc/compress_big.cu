@@ -138,7 +138,8 @@ __device__ __forceinline__ void store_tag(uint8_t *base, int64_t elem, int tag, 
     case TAG_FP64: reinterpret_cast<double *>(base)[elem] = v; break;
     case TAG_FP32: reinterpret_cast<uint32_t *>(base)[elem] = to_fp32_bits(v); break;
     case TAG_FP16: reinterpret_cast<uint16_t *>(base)[elem] = to_fp16_bits(v); break;
-    default: reinterpret_cast<uint16_t *>(base)[elem] = to_bf16_bits(v);
+    case TAG_BF16: reinterpret_cast<uint16_t *>(base)[elem] = to_bf16_bits(v); break;
+    default: base[elem] = to_q43_bits(v);
   }
 }
 

@@ -19,8 +19,10 @@
 
 namespace hh {
 
-static const double kU[4] = {0x1p-53, 0x1p-24, 0x1p-11, 0x1p-8};
-static const uint32_t kBit[4] = {HH_P_FP64, HH_P_FP32, HH_P_FP16, HH_P_BF16};
+static const double kU[NTAG] = {0x1p-53, 0x1p-24, 0x1p-11, 0x1p-8, 0x1p-4};
+static const uint32_t kBit[NTAG] = {HH_P_FP64, HH_P_FP32, HH_P_FP16, HH_P_BF16, HH_P_Q43};
+// formats in decreasing unit roundoff (the order Eq. 4.4 tries them; the range guard steps right)
+static const int kByU[NTAG] = {TAG_Q43, TAG_BF16, TAG_FP16, TAG_FP32, TAG_FP64};
 
 void cluster_range(const hh_matrix *H, int l, int64_t m, int64_t &a, int64_t &n) {
   const int sh = H->d * (H->L - l);
@@ -35,13 +37,14 @@ static bool overflows(int tag, double x) {
     case TAG_FP32: return (to_fp32_bits(x) & 0x7FFFFFFFu) == 0x7F800000u;
     case TAG_FP16: return (to_fp16_bits(x) & 0x7FFFu) == 0x7C00u;
     case TAG_BF16: return (to_bf16_bits(x) & 0x7FFFu) == 0x7F80u;
+    case TAG_Q43: return (to_q43_bits(x) & 0x7Fu) == 0x78u;
     default: return false;
   }
 }
 
 void assign_tags(hh_matrix *H) {
   const size_t nb = H->level.size();
-  const bool mixed = (H->pset & 0xF) != HH_P_FP64;
+  const bool mixed = (H->pset & 0x1F) != HH_P_FP64;
   // a4: global norm in canonical order
   double norm2 = 0.0;
   for (size_t b = 0; b < nb; ++b) {
@@ -56,8 +59,7 @@ void assign_tags(hh_matrix *H) {
     const int l = H->level[b];
     int tag = TAG_FP64;
     bool found = false;
-    const int order[4] = {TAG_BF16, TAG_FP16, TAG_FP32, TAG_FP64};
-    for (int t : order) {
+    for (int t : kByU) {
       if (!(H->pset & kBit[t])) continue;
       const double u = kU[t];
       if ((u * u) * std::ldexp(1.0, H->d * l) * H->nb2[b] <= rhs) {
@@ -73,9 +75,11 @@ void assign_tags(hh_matrix *H) {
     // promoted counter counts blocks, however many steps they take)
     bool promoted = false;
     while (tag != TAG_FP64 && overflows(tag, H->maxabs[b])) {
-      int nt = tag == TAG_BF16 ? TAG_FP16 : tag == TAG_FP16 ? TAG_FP32 : TAG_FP64;
-      while (nt != TAG_FP64 && !(H->pset & kBit[nt])) nt = nt == TAG_FP16 ? TAG_FP32 : TAG_FP64;
-      tag = nt;
+      int i = 0;
+      while (kByU[i] != tag) ++i;
+      do ++i;
+      while (kByU[i] != TAG_FP64 && !(H->pset & kBit[kByU[i]]));
+      tag = kByU[i];
       promoted = true;
     }
     pr += promoted;
@@ -119,7 +123,7 @@ void compute_layout(hh_matrix *H) {
     while (b < nb) {
       size_t e = b;
       while (e < nb && H->level[e] == H->level[b] && H->tgt[e] == H->tgt[b]) ++e;
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < NTAG; ++t)
         for (size_t i = b; i < e; ++i)
           if (is_lr(i) && H->tag[i] == t) {
             H->zoff[i] = z;
@@ -145,7 +149,7 @@ void compute_layout(hh_matrix *H) {
       if (H->src[a] != H->src[c]) return H->src[a] < H->src[c];
       return H->tgt[a] < H->tgt[c];
     });
-    int64_t off[4] = {0, 0, 0, 0};
+    int64_t off[NTAG] = {0, 0, 0, 0, 0};
     size_t i = 0;
     while (i < idx.size()) {
       size_t e = i;
@@ -167,46 +171,45 @@ void compute_layout(hh_matrix *H) {
       for (int64_t c0 = 0; c0 < P; c0 += W_CT) off[g] += align_up(n * std::min<int64_t>(W_CT, P - c0) * tag_bytes(g));
       i = e;
     }
-    for (int g = 0; g < 4; ++g) H->w_bytes[g] = off[g];
+    for (int g = 0; g < NTAG; ++g) H->w_bytes[g] = off[g];
   }
   // U[g]: per-leaf streams.  Column base of block b = columns of coarser levels of its
   // target's ancestors + prefix inside its (level, tgt, tag) group.
   {
     // group totals per (level, tgt, tag)
     std::vector<std::vector<int64_t>> gtot(L + 1);
-    for (int l = 0; l <= L; ++l) gtot[l].assign((size_t)4 << (d * l), 0);
+    for (int l = 0; l <= L; ++l) gtot[l].assign((size_t)NTAG << (d * l), 0);
     for (size_t b = 0; b < nb; ++b)
-      if (is_lr(b) && H->rank[b] > 0) gtot[H->level[b]][(size_t)H->tgt[b] * 4 + H->tag[b]] += H->rank[b];
+      if (is_lr(b) && H->rank[b] > 0) gtot[H->level[b]][(size_t)H->tgt[b] * NTAG + H->tag[b]] += H->rank[b];
     // coarser-level column base per (level, tgt, tag): base[l][t] = sum_{l' < l} gtot[l'][anc(t)]
     std::vector<std::vector<int64_t>> base(L + 1);
     for (int l = 0; l <= L; ++l) {
-      base[l].assign((size_t)4 << (d * l), 0);
+      base[l].assign((size_t)NTAG << (d * l), 0);
       if (l > 0)
         for (int64_t t = 0; t < (1ll << (d * l)); ++t)
-          for (int g = 0; g < 4; ++g)
-            base[l][t * 4 + g] = base[l - 1][(t >> d) * 4 + g] + gtot[l - 1][(t >> d) * 4 + g];
+          for (int g = 0; g < NTAG; ++g)
+            base[l][t * NTAG + g] = base[l - 1][(t >> d) * NTAG + g] + gtot[l - 1][(t >> d) * NTAG + g];
     }
-    std::vector<int64_t> run(4, 0);
     size_t b = 0;
     while (b < nb) {
       size_t e = b;
       while (e < nb && H->level[e] == H->level[b] && H->tgt[e] == H->tgt[b]) ++e;
-      int64_t within[4] = {0, 0, 0, 0};
+      int64_t within[NTAG] = {0, 0, 0, 0, 0};
       for (size_t i = b; i < e; ++i)
         if (is_lr(i) && H->rank[i] > 0) {
           const int g = H->tag[i];
-          H->ucol[i] = base[H->level[i]][(size_t)H->tgt[i] * 4 + g] + within[g];
+          H->ucol[i] = base[H->level[i]][(size_t)H->tgt[i] * NTAG + g] + within[g];
           within[g] += H->rank[i];
         }
       b = e;
     }
-    H->u_leaf_off.assign((size_t)4 * (ncell + 1), 0);
-    for (int g = 0; g < 4; ++g) {
+    H->u_leaf_off.assign((size_t)NTAG * (ncell + 1), 0);
+    for (int g = 0; g < NTAG; ++g) {
       int64_t off = 0;
       for (int64_t R = 0; R < ncell; ++R) {
         H->u_leaf_off[(size_t)g * (ncell + 1) + R] = off;
         const int64_t nr = H->leaf_start[R + 1] - H->leaf_start[R];
-        const int64_t cols = base[L][(size_t)R * 4 + g] + gtot[L][(size_t)R * 4 + g];
+        const int64_t cols = base[L][(size_t)R * NTAG + g] + gtot[L][(size_t)R * NTAG + g];
         off += align_up(nr * cols * tag_bytes(g));
       }
       H->u_leaf_off[(size_t)g * (ncell + 1) + ncell] = off;
@@ -234,11 +237,11 @@ void compute_layout(hh_matrix *H) {
       }
   }
   // ledger
-  int64_t tagged[5] = {0, 0, 0, 0, 0};
+  int64_t tagged[NTAG + 1] = {0, 0, 0, 0, 0, 0};
   int64_t nlr = 0, nd = 0;
   for (size_t b = 0; b < nb; ++b) {
     if (H->storage[b] == STORE_DENSE) {
-      tagged[4] += M[b] * Nn[b] * 8;
+      tagged[NTAG] += M[b] * Nn[b] * 8;
       ++nd;
     } else {
       tagged[H->tag[b]] += (int64_t)H->rank[b] * (M[b] + Nn[b]) * tag_bytes(H->tag[b]);
@@ -246,11 +249,11 @@ void compute_layout(hh_matrix *H) {
     }
   }
   int64_t tot = 0, pad = H->d_bytes;
-  for (int i = 0; i < 5; ++i) {
+  for (int i = 0; i <= NTAG; ++i) {
     H->info.stored_bytes_tag[i] = tagged[i];
     tot += tagged[i];
   }
-  for (int g = 0; g < 4; ++g) pad += H->w_bytes[g] + H->u_bytes[g];
+  for (int g = 0; g < NTAG; ++g) pad += H->w_bytes[g] + H->u_bytes[g];
   H->info.stored_bytes = tot;
   H->info.padded_bytes = pad;
   H->info.n_lowrank = nlr;
@@ -333,12 +336,12 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
   // ---- phase 2: group (level, tgt, tag) -> (zbeg, P)
   std::vector<std::vector<int64_t>> gz(L + 1), gp(L + 1);
   for (int l = 0; l <= L; ++l) {
-    gz[l].assign((size_t)4 << (d * l), -1);
-    gp[l].assign((size_t)4 << (d * l), 0);
+    gz[l].assign((size_t)NTAG << (d * l), -1);
+    gp[l].assign((size_t)NTAG << (d * l), 0);
   }
   for (size_t b = 0; b < nb; ++b)
     if (H->storage[b] == STORE_LR && H->rank[b] > 0) {
-      const size_t key = (size_t)H->tgt[b] * 4 + H->tag[b];
+      const size_t key = (size_t)H->tgt[b] * NTAG + H->tag[b];
       if (gz[H->level[b]][key] < 0) gz[H->level[b]][key] = H->zoff[b];
       gp[H->level[b]][key] += H->rank[b];
     }
@@ -357,12 +360,12 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
       segs.push_back(P2Seg{H->d_off[b], j0, (int32_t)n, (int16_t)TAG_FP64, 1});
       bytes += nr * n * 8;
     }
-    for (int g = 0; g < 4; ++g) {
+    for (int g = 0; g < NTAG; ++g) {
       const int w = tag_bytes(g);
       int64_t col = 0;
       const int64_t base = H->u_leaf_off[(size_t)g * (H->ncell + 1) + R];
       for (int l = 0; l <= L; ++l) {
-        const size_t key = (size_t)(R >> (d * (L - l))) * 4 + g;
+        const size_t key = (size_t)(R >> (d * (L - l))) * NTAG + g;
         const int64_t P = gp[l][key];
         if (P == 0) continue;
         segs.push_back(P2Seg{base + col * nr * w, N + gz[l][key], (int32_t)P, (int16_t)g, 0});

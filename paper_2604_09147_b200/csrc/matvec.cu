@@ -173,8 +173,8 @@ __device__ __forceinline__ int stage_copy(uint8_t *dst, const uint8_t *src, int6
   return (int)(s - sa);
 }
 // arena base by tag without dynamic indexing of the kernel-parameter array (no local memory)
-__device__ __forceinline__ const uint8_t *pick(const uint8_t *const (&arr)[4], int t) {
-  return t == 0 ? arr[0] : t == 1 ? arr[1] : t == 2 ? arr[2] : arr[3];
+__device__ __forceinline__ const uint8_t *pick(const uint8_t *const (&arr)[NTAG], int t) {
+  return t == 0 ? arr[0] : t == 1 ? arr[1] : t == 2 ? arr[2] : t == 3 ? arr[3] : arr[4];
 }
 __device__ __forceinline__ uint32_t window_bytes(const uint8_t *src, int64_t bytes) {
   const uintptr_t s = (uintptr_t)src;
@@ -186,6 +186,7 @@ template <> struct Elem<TAG_FP64> { using T = double; };
 template <> struct Elem<TAG_FP32> { using T = float; };
 template <> struct Elem<TAG_FP16> { using T = __half; };
 template <> struct Elem<TAG_BF16> { using T = uint16_t; };
+template <> struct Elem<TAG_Q43> { using T = uint8_t; };
 
 // Tunables (compile-time; scripts/variants.sh builds alternatives side by side).
 #ifndef HH_MV_CVT
@@ -197,6 +198,11 @@ template <int TAG>
 __device__ __forceinline__ double up(const typename Elem<TAG>::T v) {
   if constexpr (TAG == TAG_FP64) {
     return v;
+  } else if constexpr (TAG == TAG_Q43) {
+    // q43 byte s|eeee|mmm (bias 7) placed in an fp16's top bits (exponent field 0eeee, mantissa
+    // mmm0000000) is the same value scaled by 2^-8, normals and subnormals alike: exact
+    const uint32_t b = v;
+    return (double)__half2float(__ushort_as_half((unsigned short)(((b & 0x80u) << 8) | ((b & 0x7Fu) << 7)))) * 256.0;
   } else if constexpr (HH_MV_CVT == 1) {
     // place sign / exponent / mantissa bits in an fp64 with the same (unbiased-shifted)
     // exponent field, then rescale by the exact power of two between the two biases
@@ -264,7 +270,7 @@ struct P1Args {
   const int32_t *zmap;
   double *partial;    // [npartial] x NR partial column sums of row-split tiles
   int64_t ntiles;
-  const uint8_t *W[4];
+  const uint8_t *W[NTAG];
   double *v;          // [x~ (N) ; z] x NR
   int64_t N;
   int *ctr;
@@ -399,7 +405,8 @@ __device__ __forceinline__ void p1_mma_consumer(const P1Args &a, uint8_t *smem, 
         case TAG_FP64: p1_mma_rows<TAG_FP64, NR>(wst, xst, nrows, ct, col0, lane, c); break;
         case TAG_FP32: p1_mma_rows<TAG_FP32, NR>(wst, xst, nrows, ct, col0, lane, c); break;
         case TAG_FP16: p1_mma_rows<TAG_FP16, NR>(wst, xst, nrows, ct, col0, lane, c); break;
-        default: p1_mma_rows<TAG_BF16, NR>(wst, xst, nrows, ct, col0, lane, c); break;
+        case TAG_BF16: p1_mma_rows<TAG_BF16, NR>(wst, xst, nrows, ct, col0, lane, c); break;
+        default: p1_mma_rows<TAG_Q43, NR>(wst, xst, nrows, ct, col0, lane, c); break;
       }
     }
     __syncwarp();
@@ -542,9 +549,13 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
           block_acc<TAG_FP16, NR, MB>(reinterpret_cast<const __half *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
                                       Q * NR, valid, acc);
           break;
-        default:
+        case TAG_BF16:
           block_acc<TAG_BF16, NR, MB>(reinterpret_cast<const uint16_t *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
                                       Q * NR, valid, acc);
+          break;
+        default:
+          block_acc<TAG_Q43, NR, MB>(reinterpret_cast<const uint8_t *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
+                                     Q * NR, valid, acc);
           break;
       }
     }
@@ -573,7 +584,7 @@ struct P2Args {
   const P2Leaf *leaves;
   const P2Seg *segs;
   int64_t nleaves;
-  const uint8_t *U[4];
+  const uint8_t *U[NTAG];
   const uint8_t *D;
   const double *v;
   const int32_t *perm;
@@ -684,7 +695,8 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
         case TAG_FP64: p2_mma_cols<TAG_FP64, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
         case TAG_FP32: p2_mma_cols<TAG_FP32, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
         case TAG_FP16: p2_mma_cols<TAG_FP16, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
-        default: p2_mma_cols<TAG_BF16, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
+        case TAG_BF16: p2_mma_cols<TAG_BF16, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
+        default: p2_mma_cols<TAG_Q43, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
       }
     }
     if (KS == 1) {
@@ -860,9 +872,13 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
           block_acc<TAG_FP16, NR, MB>(reinterpret_cast<const __half *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
                                       Gn * NR, valid, acc);
           break;
-        default:
+        case TAG_BF16:
           block_acc<TAG_BF16, NR, MB>(reinterpret_cast<const uint16_t *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
                                       Gn * NR, valid, acc);
+          break;
+        default:
+          block_acc<TAG_Q43, NR, MB>(reinterpret_cast<const uint8_t *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
+                                     Gn * NR, valid, acc);
           break;
       }
     }
@@ -944,7 +960,7 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     a.zmap = H->zmap.as<int32_t>();
     a.partial = H->partial.as<double>();
     a.ntiles = H->n_p1_tiles;
-    for (int g = 0; g < 4; ++g) a.W[g] = H->W[g].as<uint8_t>();
+    for (int g = 0; g < NTAG; ++g) a.W[g] = H->W[g].as<uint8_t>();
     a.v = v;
     a.N = H->N;
     a.ctr = ctr;
@@ -962,7 +978,7 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   b.leaves = H->p2_leaves.as<P2Leaf>();
   b.segs = H->p2_segs.as<P2Seg>();
   b.nleaves = H->n_p2_leaves;
-  for (int g = 0; g < 4; ++g) b.U[g] = H->U[g].as<uint8_t>();
+  for (int g = 0; g < NTAG; ++g) b.U[g] = H->U[g].as<uint8_t>();
   b.D = H->D.as<uint8_t>();
   b.v = v;
   b.perm = H->d_perm.as<int32_t>();

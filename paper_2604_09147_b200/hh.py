@@ -16,12 +16,13 @@ LIB_PATH = os.environ.get("HH_LIB") or os.path.join(_HERE, "libhh.so")   # HH_LI
 
 HH_OK, HH_EINVAL, HH_ENOMEM, HH_ECUDA, HH_ENUMERIC, HH_EDEPTH, HH_EUNSUPPORTED = range(7)
 K_LOG, K_INV_R, K_INV_R2, K_GAUSS, K_EXP = range(5)
-P_FP64, P_FP32, P_FP16, P_BF16 = 1, 2, 4, 8
+P_FP64, P_FP32, P_FP16, P_BF16, P_Q43 = 1, 2, 4, 8, 16
 P_MIXED = 15
+NTAG = 5                                   # tags 0..4 = fp64, fp32, fp16, bf16, q43
 LEDGER_ONLY = 1 << 16
 TIE_FP16 = 1 << 17
 SWITCH_NONE = -1
-ARENA_W, ARENA_U, ARENA_D = 0, 4, 8
+ARENA_W, ARENA_U, ARENA_D = 0, 5, 10
 
 
 class HHError(RuntimeError):
@@ -41,8 +42,8 @@ class hh_info_t(C.Structure):
         ("precision_set", C.c_uint32), ("ledger_only", C.c_int32),
         ("n_cells", C.c_int64), ("nblocks", C.c_int64), ("n_lowrank", C.c_int64), ("n_dense", C.c_int64),
         ("total_rank", C.c_int64), ("norm2", C.c_double),
-        ("w_bytes", C.c_int64 * 4), ("u_bytes", C.c_int64 * 4), ("d_bytes", C.c_int64),
-        ("stored_bytes", C.c_int64), ("stored_bytes_tag", C.c_int64 * 5), ("padded_bytes", C.c_int64),
+        ("w_bytes", C.c_int64 * 5), ("u_bytes", C.c_int64 * 5), ("d_bytes", C.c_int64),
+        ("stored_bytes", C.c_int64), ("stored_bytes_tag", C.c_int64 * 6), ("padded_bytes", C.c_int64),
         ("c_far", C.c_int32), ("c_nbr", C.c_int32), ("c_sib", C.c_int32),
         ("n_fallback", C.c_int64), ("n_promoted", C.c_int64), ("n_coincident", C.c_int64), ("n_retry", C.c_int64),
         ("build_seconds", C.c_double), ("n_inexact", C.c_int64),
@@ -187,14 +188,14 @@ def hh_export(H: Handle, tables: bool = True, arenas: bool = True) -> dict:
         perm = np.empty(info["N"], np.int32)
         ls = np.empty(info["n_cells"] + 1, np.int64)
         blocks = np.empty(info["nblocks"], BLOCK_DTYPE)
-        uoff = np.empty(4 * (info["n_cells"] + 1), np.int64)
+        uoff = np.empty(NTAG * (info["n_cells"] + 1), np.int64)
         doff = np.empty(info["n_cells"] + 1, np.int64)
         e.perm, e.leaf_start, e.blocks = perm.ctypes.data, ls.ctypes.data, blocks.ctypes.data
         e.u_leaf_off, e.d_leaf_off = uoff.ctypes.data, doff.ctypes.data
         _check(lib.hh_export(H.ptr, C.byref(e)))
-        out.update(perm=perm, leaf_start=ls, blocks=blocks, u_leaf_off=uoff.reshape(4, -1), d_leaf_off=doff)
+        out.update(perm=perm, leaf_start=ls, blocks=blocks, u_leaf_off=uoff.reshape(NTAG, -1), d_leaf_off=doff)
     if arenas and not info["ledger_only"]:
-        for g in range(4):
+        for g in range(NTAG):
             out[("W", g)] = export_arena(H, ARENA_W + g, 0, info["w_bytes"][g])
             out[("U", g)] = export_arena(H, ARENA_U + g, 0, info["u_bytes"][g])
         out["D"] = export_arena(H, ARENA_D, 0, info["d_bytes"])
@@ -261,15 +262,15 @@ def selftest_layout(leaf_start, d, L, level, tgt, src, rank, tag, storage) -> di
     st = np.ascontiguousarray(storage, dtype=np.uint8)
     nb, ncell = lv.size, ls.size - 1
     out = {k: np.empty(nb, np.int64) for k in ("zoff", "w_off", "wcol", "ucol", "d_off")}
-    out["u_leaf_off"] = np.empty(4 * (ncell + 1), np.int64)
+    out["u_leaf_off"] = np.empty(NTAG * (ncell + 1), np.int64)
     out["d_leaf_off"] = np.empty(ncell + 1, np.int64)
-    out["w_bytes"] = np.empty(4, np.int64)
+    out["w_bytes"] = np.empty(NTAG, np.int64)
     _check(lib.hh_selftest_layout(ls.ctypes.data, d, L, nb, lv.ctypes.data, tg.ctypes.data, sr.ctypes.data,
                                   rk.ctypes.data, ta.ctypes.data, st.ctypes.data, out["zoff"].ctypes.data,
                                   out["w_off"].ctypes.data, out["wcol"].ctypes.data, out["ucol"].ctypes.data,
                                   out["d_off"].ctypes.data, out["u_leaf_off"].ctypes.data,
                                   out["d_leaf_off"].ctypes.data, out["w_bytes"].ctypes.data))
-    out["u_leaf_off"] = out["u_leaf_off"].reshape(4, -1)
+    out["u_leaf_off"] = out["u_leaf_off"].reshape(NTAG, -1)
     return out
 
 

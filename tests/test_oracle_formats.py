@@ -10,7 +10,7 @@ from oracle import formats as F
 
 def test_unit_roundoffs_match_table1():
     # PAPER.md:42-45 prints u rounded to 3 significant digits
-    printed = {F.FP64: 1.11e-16, F.FP32: 5.96e-8, F.FP16: 4.88e-4, F.BF16: 3.91e-3}
+    printed = {F.FP64: 1.11e-16, F.FP32: 5.96e-8, F.FP16: 4.88e-4, F.BF16: 3.91e-3}   # q43: see below
     for t, u in printed.items():
         assert abs(F.unit_roundoff(t) - u) / u < 5e-3
 
@@ -100,3 +100,70 @@ def test_storage_bits_roundtrip():
         b = F.to_storage_bits(x, t)
         back = F.from_storage_bytes(b.tobytes(), t)
         np.testing.assert_array_equal(back, F.round_rne(x, t))
+
+
+# ------------------------------------------------------------- q43 (Table 1, 8-bit; NEXT-3)
+def _q43_values():
+    """Every finite non-negative q43 value from Table 1's definition (1-4-3, e_min -6, e_max 7,
+    exponent field 15 reserved): (1 + m/8) 2^(e-7) for e = 1..14, (m/8) 2^-6 for e = 0."""
+    vals, bits = [], []
+    for e in range(15):
+        for m in range(8):
+            vals.append(Fraction(m, 8) * Fraction(1, 64) if e == 0 else (1 + Fraction(m, 8)) * Fraction(2) ** (e - 7))
+            bits.append(e << 3 | m)
+    order = sorted(range(len(vals)), key=lambda i: vals[i])
+    return [vals[i] for i in order], [bits[i] for i in order]
+
+
+def test_q43_table1_row():
+    assert F.x_max(F.Q43) == 240.0                                   # Table 1: 2.4e2
+    assert F.PARAMS[F.Q43] == (3, -6, 7) and 2.0 ** -6 == 0.015625    # x_min 1.56e-2, e_min -6, e_max 7
+    # Table 1 prints u = 2.5e-1 for q43; reading G12: u = 2^-(m+1) = 2^-4
+    assert F.unit_roundoff(F.Q43) == 0.0625
+    assert F.BYTES[F.Q43] == 1 and F.TAG_BIT[F.Q43] == 16
+
+
+def test_q43_worked_examples():
+    r = F.round_rne(np.array([0.1, 247.99, 248.0, 2.0 ** -10, 3 * 2.0 ** -10, 1.0625, 1.1875, -0.3]), F.Q43)
+    # 0.1 = 1.6 * 2^-4 -> 1.625 * 2^-4; 248 is the midpoint 240|256 -> even (256) = overflow;
+    # 2^-10 ties between 0 and 2^-9 -> 0 (even); 3 * 2^-10 ties 2^-9|2^-8 -> 2^-8 (mantissa 2, even);
+    # 1.0625 ties 1|1.125 -> 1; 1.1875 ties 1.125|1.25 -> 1.25; -0.3 = -1.2 * 2^-2 -> -1.25 * 2^-2
+    np.testing.assert_array_equal(r, [0.1015625, 240.0, np.inf, 0.0, 2.0 ** -8, 1.0, 1.25, -0.3125])
+
+
+def test_q43_rne_matches_bruteforce_enumeration():
+    vals, bits = _q43_values()
+    rng = np.random.default_rng(11)
+    xs = []
+    for i in range(len(vals) - 1):
+        mid = (vals[i] + vals[i + 1]) / 2
+        xs += [float(mid), float(np.nextafter(float(mid), 0)), float(np.nextafter(float(mid), np.inf)), float(vals[i])]
+    xs += list(rng.uniform(0, 260, 300)) + list(rng.uniform(0, 0.05, 300))
+    got = F.round_rne(np.array(xs), F.Q43)
+    top = vals[-1] + (vals[-1] - vals[-2]) / 2          # 248: at and above -> inf (ties to even 256)
+    for x, g in zip(xs, got):
+        fx = Fraction(x)
+        if fx >= top:
+            assert np.isinf(g), x
+            continue
+        best = min(range(len(vals)), key=lambda j: (abs(vals[j] - fx), bits[j] & 1))
+        assert Fraction(float(g)) == vals[best], (x, g, vals[best])
+
+
+def test_q43_storage_bits_roundtrip_and_e4m3_decode():
+    """The q43 byte layout (sign | 4-bit exponent | 3-bit mantissa, bias 7) round-trips, and every
+    finite q43 byte decodes to the same value under the OCP FP8 E4M3 rules (torch.float8_e4m3fn,
+    a library decoder) — what lets the device use E4M3 conversions."""
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal(3000) * np.exp2(rng.integers(-12, 8, 3000))
+    r = F.round_rne(x, F.Q43)
+    x = x[np.isfinite(r)]
+    b = F.to_storage_bits(x, F.Q43)
+    np.testing.assert_array_equal(F.from_storage_bytes(b.tobytes(), F.Q43), F.round_rne(x, F.Q43))
+    torch = pytest.importorskip("torch")
+    allb = np.array([s << 7 | e << 3 | m for s in (0, 1) for e in range(15) for m in range(8)], np.uint8)
+    ours = F.from_storage_bytes(allb.tobytes(), F.Q43)
+    ocp = torch.from_numpy(allb.copy()).view(torch.float8_e4m3fn).to(torch.float64).numpy()
+    np.testing.assert_array_equal(ours, ocp)
+    vals, _ = _q43_values()
+    np.testing.assert_array_equal(np.sort(np.unique(np.abs(ours))), np.array([float(v) for v in vals]))

@@ -217,8 +217,8 @@ def test_pack_roundtrip_and_invariants(tiny_oracle):
     tr, part = H.tree, H.part
     lay = PK.pack(tr.leaf_start, tr.d, tr.L, part.level, part.tgt, part.src, H.rank, H.tag, H.storage)
     # write every block into byte arenas with the layout, then unpack it again
-    arenas = {("W", g): np.zeros(int(lay["w_bytes"][g]), np.uint8) for g in range(4)}
-    arenas.update({("U", g): np.zeros(int(lay["u_leaf_off"][g, -1]), np.uint8) for g in range(4)})
+    arenas = {("W", g): np.zeros(int(lay["w_bytes"][g]), np.uint8) for g in F.TAGS}
+    arenas.update({("U", g): np.zeros(int(lay["u_leaf_off"][g, -1]), np.uint8) for g in F.TAGS})
     arenas["D"] = np.zeros(int(lay["d_leaf_off"][-1]), np.uint8)
     used = {k: np.zeros(v.size, np.int32) for k, v in arenas.items()}
 
@@ -253,7 +253,7 @@ def test_pack_roundtrip_and_invariants(tiny_oracle):
     assert np.any(lay["wpanel"] > PK.CT)  # multi-tile W panels are exercised
     for k in used:                      # no byte written twice
         assert used[k].max(initial=0) <= 1
-    for g in range(4):
+    for g in F.TAGS:
         assert np.all(lay["u_leaf_off"][g] % 16 == 0)
     for b in range(len(part)):
         kind, payload = PK.unpack_block(lay, b, tr.leaf_start, tr.d, tr.L, part.level, part.tgt,

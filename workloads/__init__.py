@@ -122,3 +122,9 @@ def make_points(cfg: dict) -> np.ndarray:
 
 def make_rhs(cfg: dict, nrhs: int | None = None) -> np.ndarray:
     return rhs(cfg["N"], nrhs or cfg["nrhs"], 2000 + cfg["k"], cfg["xdist"])
+
+# NEXT-3: Table 1's 8-bit q43 as an extra storage format (precision_set bit 16, include/hh.h)
+P_Q43 = 16
+P_MIXED_Q43 = P_MIXED | P_Q43
+SMALL_CONFIGS["2d_fig8_e2_q43"] = dict(SMALL_CONFIGS["2d_fig8_e2"], k=17, pset=P_MIXED_Q43)
+SMALL_CONFIGS["3d_small_exp_q43"] = dict(SMALL_CONFIGS["3d_small_exp"], k=18, eps=1e-3, pset=P_MIXED_Q43)
