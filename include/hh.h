@@ -133,6 +133,22 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
 hh_status hh_matvec(hh_handle H, const double *x, double *y, int32_t nrhs, void *cuda_stream);
 
 /*
+ * hh_matvec_wp — Alg. 3 in a lower working precision u (NEXT-3: the backward-error study of
+ * PAPER.md:1266-1285, Thm 4.4 at PAPER.md:1028-1040, "this u may differ from the u used in
+ * Alg. 2").  Reading G27: x and every stored factor / dense entry enter rounded
+ * once (RNE) to the working format (exact when the storage format is narrower), every
+ * multiply-add is one fused multiply-add rounded to it, z and all partial sums are held in it,
+ * and y receives its working-precision values as float64.  The summation order is the
+ * library's (fixed, deterministic; the paper fixes none).  Arguments as hh_matvec;
+ * working_precision = HH_WP_FP64 (identical to hh_matvec), HH_WP_FP32 or HH_WP_FP16.  Reduced
+ * precisions run chunks of <= 4 columns on the FMA pipes (no FP64 tensor cores).
+ * Errors: as hh_matvec; HH_EINVAL for an unknown working_precision.
+ */
+enum { HH_WP_FP64 = 0, HH_WP_FP32 = 1, HH_WP_FP16 = 2 };
+hh_status hh_matvec_wp(hh_handle H, const double *x, double *y, int32_t nrhs, int32_t working_precision,
+                       void *cuda_stream);
+
+/*
  * hh_matvec_host — same product with HOST x and y: copies x host->device, runs hh_matvec
  * and copies y device->host on `stream`, then synchronises it (the end-to-end path).
  */

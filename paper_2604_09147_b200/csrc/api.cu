@@ -334,6 +334,31 @@ hh_status hh_matvec(hh_handle H, const double *x, double *y, int32_t nrhs, void 
   }
 }
 
+hh_status hh_matvec_wp(hh_handle H, const double *x, double *y, int32_t nrhs, int32_t working_precision,
+                       void *cuda_stream) {
+  g_err.clear();
+  if (working_precision < HH_WP_FP64 || working_precision > HH_WP_FP16)
+    return fail(HH_EINVAL, "working_precision must be HH_WP_FP64, HH_WP_FP32 or HH_WP_FP16");
+  if (!H || !x || !y) return fail(HH_EINVAL, "NULL pointer");
+  if (nrhs < 1) return fail(HH_EINVAL, "nrhs must be >= 1");
+  if (H->ledger) return fail(HH_EINVAL, "ledger-only handle has no factors");
+  const char *xb = (const char *)x, *yb = (const char *)y;
+  const size_t bytes = sizeof(double) * (size_t)H->N * nrhs;
+  if (!(xb + bytes <= yb || yb + bytes <= xb)) return fail(HH_EINVAL, "x and y overlap");
+  try {
+    run_matvec(H, x, y, nrhs, (cudaStream_t)cuda_stream, working_precision);
+    return HH_OK;
+  } catch (const Error &e) {
+    return fail(e.st, e.what());
+  } catch (const std::bad_alloc &) {
+    return fail(HH_ENOMEM, "host allocation failed");
+  } catch (const std::exception &e) {
+    return fail(HH_ECUDA, e.what());
+  } catch (...) {
+    return fail(HH_ECUDA, "unexpected error");
+  }
+}
+
 hh_status hh_matvec_host(hh_handle H, const double *x_host, double *y_host, int32_t nrhs, void *cuda_stream) {
   g_err.clear();
   if (!H || !x_host || !y_host) return fail(HH_EINVAL, "NULL pointer");

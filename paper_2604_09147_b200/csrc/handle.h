@@ -113,7 +113,7 @@ struct hh_matrix {
   struct LaunchCfg {  // per RHS-chunk width (1, 2, 4, 8, 16): set once, reused by every hh_matvec
     bool ready = false;
     int nsm = 0, grid1 = 0, grid2 = 0;
-  } lcfg[5];
+  } lcfg[3][5];  // [working precision][width]
   hh::DBuf hx, hy;   // staging for hh_matvec_host
   // optional per-phase timing of the matvec (hh_matvec_profile)
   bool prof = false;

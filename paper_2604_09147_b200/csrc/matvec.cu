@@ -21,6 +21,7 @@
 // small descriptor, so the 8 consumer warps never touch global memory in their inner loops.
 // Consumers: fp64 FMA (DFMA) at NR = 1, 2, 4; FP64 tensor cores (DMMA) at NR = 8, 16.
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "build.h"
@@ -232,34 +233,95 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// --------------------------------------------------------------------------- working precision
+// Alg. 3 "compute in working precision u" with u below fp64 — the paper's
+// backward-error study (Thm 4.4).  Reading G27: x and every
+// stored factor / dense entry enter rounded once (RNE) to the working format; every
+// multiply-add is one FMA rounded to it; partial sums, z and the cross-thread reductions are
+// held in it; y returns its working-precision values as fp64.  WP 0 = fp64 is the product path
+// (the code below reduces to it exactly), 1 = fp32 (FFMA), 2 = fp16 (HFMA).
+template <int WP> struct WpT;
+template <> struct WpT<0> { using A = double; };
+template <> struct WpT<1> { using A = float; };
+template <> struct WpT<2> { using A = __half; };
+
+template <class A> __device__ __forceinline__ A wp_round(double v) {
+  if constexpr (std::is_same_v<A, double>) return v;
+  else if constexpr (std::is_same_v<A, float>) return __double2float_rn(v);
+  else return __double2half(v);  // cvt.rn.f16.f64: one RNE rounding
+}
+template <class A> __device__ __forceinline__ double wp_out(A v) {
+  if constexpr (std::is_same_v<A, __half>) return (double)__half2float(v);
+  else return (double)v;
+}
+template <class A> __device__ __forceinline__ A wp_zero() {
+  if constexpr (std::is_same_v<A, __half>) return __ushort_as_half((unsigned short)0);
+  else return A(0);
+}
+template <class A> __device__ __forceinline__ A wp_fma(A a, A b, A c) {
+  if constexpr (std::is_same_v<A, double>) return __fma_rn(a, b, c);
+  else if constexpr (std::is_same_v<A, float>) return __fmaf_rn(a, b, c);
+  else return __hfma(a, b, c);
+}
+template <class A> __device__ __forceinline__ A wp_add(A a, A b) {
+  if constexpr (std::is_same_v<A, double>) return a + b;
+  else if constexpr (std::is_same_v<A, float>) return __fadd_rn(a, b);
+  else return __hadd(a, b);
+}
+// a stored element of format TAG as a working-precision operand (one RNE rounding when the
+// storage format is wider than the working one; exact otherwise)
+template <int TAG, class A> __device__ __forceinline__ A wp_elem(const typename Elem<TAG>::T v) {
+  if constexpr (std::is_same_v<A, double>) {
+    return up<TAG>(v);
+  } else if constexpr (std::is_same_v<A, float>) {
+    if constexpr (TAG == TAG_FP64) return __double2float_rn(v);
+    else if constexpr (TAG == TAG_FP32) return v;
+    else if constexpr (TAG == TAG_FP16) return __half2float(v);
+    else if constexpr (TAG == TAG_BF16) return __uint_as_float(((uint32_t)v) << 16);
+    else return (float)up<TAG_Q43>(v);
+  } else {
+    if constexpr (TAG == TAG_FP64) return __double2half(v);
+    else if constexpr (TAG == TAG_FP32) return __float2half_rn(v);
+    else if constexpr (TAG == TAG_FP16) return v;
+    else if constexpr (TAG == TAG_BF16) return __float2half_rn(__uint_as_float(((uint32_t)v) << 16));
+    else {
+      const uint32_t b = v;  // q43 values are exact in fp16: bit placement then x 2^8
+      return __hmul(__ushort_as_half((unsigned short)(((b & 0x80u) << 8) | ((b & 0x7Fu) << 7))),
+                    __ushort_as_half((unsigned short)0x5C00u));
+    }
+  }
+}
+
 // --------------------------------------------------------------------------- gather
-template <int NR>
+template <int NR, int WP = 0>
 __global__ void k_gather(const int32_t *__restrict__ perm, const double *__restrict__ x, int64_t N, int64_t ldx,
                          double *__restrict__ v, int *ctr) {
+  using A = typename WpT<WP>::A;
   if (blockIdx.x == 0 && threadIdx.x < 2) ctr[threadIdx.x] = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = perm[t];
 #pragma unroll
-    for (int r = 0; r < NR; ++r) v[t * NR + r] = x[i + r * ldx];
+    for (int r = 0; r < NR; ++r) v[t * NR + r] = wp_out<A>(wp_round<A>(x[i + r * ldx]));
   }
 }
 
 // a8 (second pass for row-split tiles): z = sum over pieces in piece order (deterministic)
-template <int NR>
+template <int NR, int WP = 0>
 __global__ void k_p1_combine(const P1Combine *__restrict__ cm, int64_t ncomb, const int32_t *__restrict__ zmap,
                              const double *__restrict__ partial, double *v, int64_t N) {
+  using A = typename WpT<WP>::A;
   for (int64_t t = blockIdx.x; t < ncomb; t += gridDim.x) {
     const P1Combine C = cm[t];
     for (int c = threadIdx.x; c < C.ct; c += blockDim.x) {
-      double s[NR];
+      A s[NR];
 #pragma unroll
-      for (int k = 0; k < NR; ++k) s[k] = 0.0;
+      for (int k = 0; k < NR; ++k) s[k] = wp_zero<A>();
       for (int q = 0; q < C.npieces; ++q)
 #pragma unroll
-        for (int k = 0; k < NR; ++k) s[k] += partial[(C.pbase + (int64_t)q * C.ct + c) * NR + k];
+        for (int k = 0; k < NR; ++k) s[k] = wp_add(s[k], wp_round<A>(partial[(C.pbase + (int64_t)q * C.ct + c) * NR + k]));
       double *out = v + (N + zmap[C.zbase + c]) * NR;
 #pragma unroll
-      for (int k = 0; k < NR; ++k) out[k] = s[k];
+      for (int k = 0; k < NR; ++k) out[k] = wp_out<A>(s[k]);
     }
   }
 }
@@ -283,30 +345,33 @@ template <int NR> constexpr int mblock() { return NR >= 8 ? 2 : 1; }
 // Strided dot-accumulate over the cnt indices j this thread owns:
 //   acc[b][k] += up(e[j * es + b * eo]) * v[j * vs + k]      (b < MB with valid[b])
 // One fixed summation order per (b, k) => bitwise reproducible.
-template <int TAG, int NR, int MB>
+template <int TAG, int NR, int MB, class A = double>
 __device__ __forceinline__ void block_acc(const typename Elem<TAG>::T *e, const double *v, int cnt, int es, int eo,
-                                          int vs, const bool (&valid)[MB], double (&acc)[MB][NR]) {
+                                          int vs, const bool (&valid)[MB], A (&acc)[MB][NR]) {
 #pragma unroll 2
   for (int j = 0; j < cnt; ++j) {
-    double a[MB];
+    A a[MB];
 #pragma unroll
-    for (int b = 0; b < MB; ++b) a[b] = valid[b] ? up<TAG>(e[b * eo]) : 0.0;
+    for (int b = 0; b < MB; ++b) a[b] = valid[b] ? wp_elem<TAG, A>(e[b * eo]) : wp_zero<A>();
     if constexpr (NR % 2 == 0) {  // 16-B aligned vector entries (NR * 8 bytes per index)
       const double2 *v2 = reinterpret_cast<const double2 *>(v);
 #pragma unroll
       for (int k2 = 0; k2 < NR / 2; ++k2) {
         const double2 xv = v2[k2];
+        const A x0 = wp_round<A>(xv.x), x1 = wp_round<A>(xv.y);  // exact: v holds working-precision values
 #pragma unroll
         for (int b = 0; b < MB; ++b) {
-          acc[b][2 * k2] = __fma_rn(a[b], xv.x, acc[b][2 * k2]);
-          acc[b][2 * k2 + 1] = __fma_rn(a[b], xv.y, acc[b][2 * k2 + 1]);
+          acc[b][2 * k2] = wp_fma(a[b], x0, acc[b][2 * k2]);
+          acc[b][2 * k2 + 1] = wp_fma(a[b], x1, acc[b][2 * k2 + 1]);
         }
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < NR; ++k)
+      for (int k = 0; k < NR; ++k) {
+        const A xk = wp_round<A>(v[k]);
 #pragma unroll
-        for (int b = 0; b < MB; ++b) acc[b][k] = __fma_rn(a[b], v[k], acc[b][k]);
+        for (int b = 0; b < MB; ++b) acc[b][k] = wp_fma(a[b], xk, acc[b][k]);
+      }
     }
     e += es;
     v += vs;
@@ -426,9 +491,11 @@ __device__ __forceinline__ void p1_mma_consumer(const P1Args &a, uint8_t *smem, 
   }
 }
 
-template <int NR>
+template <int NR, int WP = 0>
 __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
+  static_assert(WP == 0 || NR <= 4, "reduced working precision runs the FMA consumers (NR <= 4)");
   using G = Geo<NR, 1>;
+  using A = typename WpT<WP>::A;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
   uint64_t *empty = full + G::STAGES;
@@ -492,7 +559,7 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
     mbar_arrive(&full[s]);
     return;
   }
-  if constexpr (use_mma<NR>()) {
+  if constexpr (WP == 0 && use_mma<NR>()) {
     p1_mma_consumer<NR, G>(a, smem, full, empty, warp, lane);
     return;
   }
@@ -500,7 +567,7 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
   constexpr int MB = mblock<NR>();
   const int tid = threadIdx.x;
   int cur_ct = -1, slots = 1, Q = 1, cs = 0, q = 0;
-  double acc[MB][NR];
+  A acc[MB][NR];
   int32_t zi[MB];
   for (int n = 0;; ++n) {
     const int s = n % G::STAGES;
@@ -526,7 +593,7 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
 #pragma unroll
       for (int b = 0; b < MB; ++b) {
 #pragma unroll
-        for (int k = 0; k < NR; ++k) acc[b][k] = 0.0;
+        for (int k = 0; k < NR; ++k) acc[b][k] = wp_zero<A>();
         if (valid[b] && q == 0 && m.pb < 0) zi[b] = a.zmap[m.p + cs + b * slots];
       }
     }
@@ -538,23 +605,23 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
       const int e0 = q * ct + cs;
       switch (m.b) {
         case TAG_FP64:
-          block_acc<TAG_FP64, NR, MB>(reinterpret_cast<const double *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
+          block_acc<TAG_FP64, NR, MB, A>(reinterpret_cast<const double *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
                                       Q * NR, valid, acc);
           break;
         case TAG_FP32:
-          block_acc<TAG_FP32, NR, MB>(reinterpret_cast<const float *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
+          block_acc<TAG_FP32, NR, MB, A>(reinterpret_cast<const float *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
                                       Q * NR, valid, acc);
           break;
         case TAG_FP16:
-          block_acc<TAG_FP16, NR, MB>(reinterpret_cast<const __half *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
+          block_acc<TAG_FP16, NR, MB, A>(reinterpret_cast<const __half *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
                                       Q * NR, valid, acc);
           break;
         case TAG_BF16:
-          block_acc<TAG_BF16, NR, MB>(reinterpret_cast<const uint16_t *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
+          block_acc<TAG_BF16, NR, MB, A>(reinterpret_cast<const uint16_t *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
                                       Q * NR, valid, acc);
           break;
         default:
-          block_acc<TAG_Q43, NR, MB>(reinterpret_cast<const uint8_t *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
+          block_acc<TAG_Q43, NR, MB, A>(reinterpret_cast<const uint8_t *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
                                      Q * NR, valid, acc);
           break;
       }
@@ -566,14 +633,14 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
 #pragma unroll
         for (int b = 0; b < MB; ++b)
 #pragma unroll
-          for (int k = 0; k < NR; ++k) acc[b][k] += __shfl_xor_sync(0xffffffffu, acc[b][k], o);
+          for (int k = 0; k < NR; ++k) acc[b][k] = wp_add(acc[b][k], __shfl_xor_sync(0xffffffffu, acc[b][k], o));
       if (q == 0)
 #pragma unroll
         for (int b = 0; b < MB; ++b)
           if (valid[b]) {
             double *out = m.pb >= 0 ? a.partial + (m.pb + cs + b * slots) * NR : a.v + (a.N + zi[b]) * NR;
 #pragma unroll
-            for (int k = 0; k < NR; ++k) out[k] = acc[b][k];
+            for (int k = 0; k < NR; ++k) out[k] = wp_out<A>(acc[b][k]);
           }
     }
   }
@@ -753,9 +820,11 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
   }
 }
 
-template <int NR>
+template <int NR, int WP = 0>
 __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
+  static_assert(WP == 0 || NR <= 4, "reduced working precision runs the FMA consumers (NR <= 4)");
   using G = Geo<NR, 2>;
+  using A = typename WpT<WP>::A;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
   uint64_t *empty = full + G::STAGES;
@@ -823,7 +892,7 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
     mbar_arrive(&full[s]);
     return;
   }
-  if constexpr (use_mma<NR>()) {
+  if constexpr (WP == 0 && use_mma<NR>()) {
     p2_mma_consumer<NR, G>(a, smem, full, empty, red, warp, lane);
     return;
   }
@@ -831,11 +900,11 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
   constexpr int MB = mblock<NR>();
   const int tid = threadIdx.x;
   int cur_nr = -1, nr2 = 1, Gn = 1, rr = 0, g = 0;
-  double acc[MB][NR];
+  A acc[MB][NR];
 #pragma unroll
   for (int b = 0; b < MB; ++b)
 #pragma unroll
-    for (int k = 0; k < NR; ++k) acc[b][k] = 0.0;
+    for (int k = 0; k < NR; ++k) acc[b][k] = wp_zero<A>();
   for (int n = 0;; ++n) {
     const int s = n % G::STAGES;
     mbar_wait(&full[s], (n / G::STAGES) & 1);
@@ -861,23 +930,23 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
       const int e0 = g * nr + rr;
       switch (m.b & 0xff) {
         case TAG_FP64:
-          block_acc<TAG_FP64, NR, MB>(reinterpret_cast<const double *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
+          block_acc<TAG_FP64, NR, MB, A>(reinterpret_cast<const double *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
                                       Gn * NR, valid, acc);
           break;
         case TAG_FP32:
-          block_acc<TAG_FP32, NR, MB>(reinterpret_cast<const float *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
+          block_acc<TAG_FP32, NR, MB, A>(reinterpret_cast<const float *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
                                       Gn * NR, valid, acc);
           break;
         case TAG_FP16:
-          block_acc<TAG_FP16, NR, MB>(reinterpret_cast<const __half *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
+          block_acc<TAG_FP16, NR, MB, A>(reinterpret_cast<const __half *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
                                       Gn * NR, valid, acc);
           break;
         case TAG_BF16:
-          block_acc<TAG_BF16, NR, MB>(reinterpret_cast<const uint16_t *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
+          block_acc<TAG_BF16, NR, MB, A>(reinterpret_cast<const uint16_t *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
                                       Gn * NR, valid, acc);
           break;
         default:
-          block_acc<TAG_Q43, NR, MB>(reinterpret_cast<const uint8_t *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
+          block_acc<TAG_Q43, NR, MB, A>(reinterpret_cast<const uint8_t *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
                                      Gn * NR, valid, acc);
           break;
       }
@@ -888,22 +957,22 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
 #pragma unroll
       for (int b = 0; b < MB; ++b)
 #pragma unroll
-        for (int k = 0; k < NR; ++k) red[(tid * MB + b) * NR + k] = acc[b][k];
+        for (int k = 0; k < NR; ++k) red[(tid * MB + b) * NR + k] = wp_out<A>(acc[b][k]);
       consumer_sync();
       if (tid < nr2) {
 #pragma unroll
         for (int b = 0; b < MB; ++b) {
           const int r = tid + b * nr2;
           if (r < nr) {
-            double sum[NR];
+            A sum[NR];
 #pragma unroll
-            for (int k = 0; k < NR; ++k) sum[k] = 0.0;
+            for (int k = 0; k < NR; ++k) sum[k] = wp_zero<A>();
             for (int gg = 0; gg < Gn; ++gg)
 #pragma unroll
-              for (int k = 0; k < NR; ++k) sum[k] += red[((gg * nr2 + tid) * MB + b) * NR + k];
+              for (int k = 0; k < NR; ++k) sum[k] = wp_add(sum[k], wp_round<A>(red[((gg * nr2 + tid) * MB + b) * NR + k]));
             const int64_t i = a.perm[m.p + r];
 #pragma unroll
-            for (int k = 0; k < NR; ++k) a.y[i + k * a.ldy] = sum[k];
+            for (int k = 0; k < NR; ++k) a.y[i + k * a.ldy] = wp_out<A>(sum[k]);
           }
         }
       }
@@ -911,29 +980,30 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
 #pragma unroll
       for (int b = 0; b < MB; ++b)
 #pragma unroll
-        for (int k = 0; k < NR; ++k) acc[b][k] = 0.0;
+        for (int k = 0; k < NR; ++k) acc[b][k] = wp_zero<A>();
     }
   }
 }
 
 }  // namespace mv
 
-template <int NR>
+template <int NR, int WP = 0>
 void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
   using namespace mv;
   using G1 = Geo<NR, 1>;
   using G2 = Geo<NR, 2>;
-  // launch geometry (device attributes, smem opt-in, occupancy) once per handle and width
-  hh_matrix::LaunchCfg &L = H->lcfg[NR == 1 ? 0 : NR == 2 ? 1 : NR == 4 ? 2 : NR == 8 ? 3 : 4];
+  // launch geometry (device attributes, smem opt-in, occupancy) once per handle, width and
+  // working precision
+  hh_matrix::LaunchCfg &L = H->lcfg[WP][NR == 1 ? 0 : NR == 2 ? 1 : NR == 4 ? 2 : NR == 8 ? 3 : 4];
   if (!L.ready) {
     int dev = 0;
     HH_CUDA(cudaGetDevice(&dev));
     HH_CUDA(cudaDeviceGetAttribute(&L.nsm, cudaDevAttrMultiProcessorCount, dev));
-    HH_CUDA(cudaFuncSetAttribute(k_phase1<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem(false)));
-    HH_CUDA(cudaFuncSetAttribute(k_phase2<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::smem(true)));
+    HH_CUDA(cudaFuncSetAttribute(k_phase1<NR, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem(false)));
+    HH_CUDA(cudaFuncSetAttribute(k_phase2<NR, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::smem(true)));
     int p1 = 0, p2 = 0;
-    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_phase1<NR>, THREADS, G1::smem(false)));
-    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_phase2<NR>, THREADS, G2::smem(true)));
+    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_phase1<NR, WP>, THREADS, G1::smem(false)));
+    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_phase2<NR, WP>, THREADS, G2::smem(true)));
     L.grid1 = (int)std::min<int64_t>(H->n_p1_tiles, (int64_t)L.nsm * std::max(1, p1));
     L.grid2 = (int)std::min<int64_t>(H->n_p2_leaves, (int64_t)L.nsm * std::max(1, p2));
     L.ready = true;
@@ -950,7 +1020,7 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   };
   mark(0);
   // a7 gather (+ counter reset)
-  k_gather<NR><<<nsm * 8, 256, 0, st>>>(H->d_perm.as<int32_t>(), x + (int64_t)col0 * H->N, H->N, H->N, v, ctr);
+  k_gather<NR, WP><<<nsm * 8, 256, 0, st>>>(H->d_perm.as<int32_t>(), x + (int64_t)col0 * H->N, H->N, H->N, v, ctr);
   HH_LAUNCHED();
   mark(1);
   // a8 phase 1
@@ -964,10 +1034,10 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     a.v = v;
     a.N = H->N;
     a.ctr = ctr;
-    k_phase1<NR><<<(unsigned)L.grid1, THREADS, G1::smem(false), st>>>(a);
+    k_phase1<NR, WP><<<(unsigned)L.grid1, THREADS, G1::smem(false), st>>>(a);
     HH_LAUNCHED();
     if (H->n_p1_comb > 0) {
-      k_p1_combine<NR><<<(unsigned)std::min<int64_t>(H->n_p1_comb, (int64_t)nsm * 8), 256, 0, st>>>(
+      k_p1_combine<NR, WP><<<(unsigned)std::min<int64_t>(H->n_p1_comb, (int64_t)nsm * 8), 256, 0, st>>>(
           H->p1_comb.as<P1Combine>(), H->n_p1_comb, a.zmap, a.partial, v, H->N);
       HH_LAUNCHED();
     }
@@ -986,13 +1056,34 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   b.ldy = H->N;
   b.ctr = ctr;
   if (L.grid2 > 0) {
-    k_phase2<NR><<<(unsigned)L.grid2, THREADS, G2::smem(true), st>>>(b);
+    k_phase2<NR, WP><<<(unsigned)L.grid2, THREADS, G2::smem(true), st>>>(b);
     HH_LAUNCHED();
   }
   mark(3);
 }
 
-void run_matvec(hh_matrix *H, const double *x, double *y, int nrhs, cudaStream_t st) {
+template <int WP>
+void run_matvec_wp(hh_matrix *H, const double *x, double *y, int nrhs, cudaStream_t st) {
+  // reduced working precision: FMA consumers only, chunks of <= 4 columns
+  int col = 0;
+  while (col < nrhs) {
+    const int rem = nrhs - col;
+    if (rem >= 4) {
+      matvec_chunk<4, WP>(H, x, y, col, st);
+      col += 4;
+    } else if (rem >= 2) {
+      matvec_chunk<2, WP>(H, x, y, col, st);
+      col += 2;
+    } else {
+      matvec_chunk<1, WP>(H, x, y, col, st);
+      col += 1;
+    }
+  }
+}
+
+void run_matvec(hh_matrix *H, const double *x, double *y, int nrhs, cudaStream_t st, int wp) {
+  if (wp == 1) return run_matvec_wp<1>(H, x, y, nrhs, st);
+  if (wp == 2) return run_matvec_wp<2>(H, x, y, nrhs, st);
   int col = 0;
   while (col < nrhs) {
     const int rem = nrhs - col;

@@ -82,6 +82,7 @@ def _load():
                              C.c_int32, C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]
     lib.hh_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
     lib.hh_matvec_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+    lib.hh_matvec_wp.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
     lib.hh_info.argtypes = [C.c_void_p, C.POINTER(hh_info_t)]
     lib.hh_export.argtypes = [C.c_void_p, C.POINTER(hh_export_t)]
     lib.hh_free.argtypes = [C.c_void_p]
@@ -98,7 +99,7 @@ def _load():
     lib.hh_selftest_round.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]
     lib.hh_matvec_profile.argtypes = [C.c_void_p, C.c_int32]
     lib.hh_matvec_timing.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
-    for f in ("hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_selftest_round",
+    for f in ("hh_build", "hh_matvec", "hh_matvec_host", "hh_matvec_wp", "hh_info", "hh_export", "hh_free", "hh_selftest_round",
               "hh_matvec_profile", "hh_matvec_timing", "hh_switch_level_search", "hh_selftest_partition",
               "hh_selftest_layout", "hh_selftest_tags"):
         getattr(lib, f).restype = C.c_int
@@ -106,7 +107,7 @@ def _load():
 
 
 lib = _load()
-EXPORTED = ["hh_build", "hh_matvec", "hh_matvec_host", "hh_info", "hh_export", "hh_free", "hh_last_error",
+EXPORTED = ["hh_build", "hh_matvec", "hh_matvec_host", "hh_matvec_wp", "hh_info", "hh_export", "hh_free", "hh_last_error",
             "hh_kernel_launches", "hh_selftest_round", "hh_matvec_profile", "hh_matvec_timing",
             "hh_switch_level_search", "hh_selftest_partition", "hh_selftest_layout", "hh_selftest_tags"]
 
@@ -161,6 +162,19 @@ def hh_matvec(H: Handle, x, y, nrhs: int | None = None, stream=None):
     if x.dim() == 2:
         assert x.stride(0) == 1 and y.stride(0) == 1, "x/y must be column-major (N, nrhs)"
     _check(lib.hh_matvec(H.ptr, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), nrhs, _stream_ptr(stream)))
+
+
+WP_FP64, WP_FP32, WP_FP16 = 0, 1, 2
+
+
+def hh_matvec_wp(H: Handle, x, y, working_precision: int, nrhs: int | None = None, stream=None):
+    """hh_matvec in a lower working precision (WP_FP32 / WP_FP16); same tensor conventions."""
+    nrhs = nrhs or (1 if x.dim() == 1 else x.shape[1])
+    assert x.is_cuda and y.is_cuda
+    if x.dim() == 2:
+        assert x.stride(0) == 1 and y.stride(0) == 1, "x/y must be column-major (N, nrhs)"
+    _check(lib.hh_matvec_wp(H.ptr, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), nrhs, working_precision,
+                            _stream_ptr(stream)))
 
 
 def hh_matvec_host(H: Handle, x: np.ndarray, y: np.ndarray | None = None, stream=None) -> np.ndarray:

@@ -128,3 +128,15 @@ P_Q43 = 16
 P_MIXED_Q43 = P_MIXED | P_Q43
 SMALL_CONFIGS["2d_fig8_e2_q43"] = dict(SMALL_CONFIGS["2d_fig8_e2"], k=17, pset=P_MIXED_Q43)
 SMALL_CONFIGS["3d_small_exp_q43"] = dict(SMALL_CONFIGS["3d_small_exp"], k=18, eps=1e-3, pset=P_MIXED_Q43)
+
+# NEXT-3 backward-error study (Fig. 9): 3D 1/r on P_square = [-1,1]^3,
+# x ~ U(0,1); L = 2 at N = 8000 and L = 3 at N = 64000 (n_max = 125 in the paper's balanced
+# formula; the depth rule of reading G1 gives those depths with leaf 250), ell = L - 1,
+# eta = sqrt(3) (the paper's 3D setting); eps swept by the experiment.
+FIG9_CONFIGS = {
+    "3d_fig9_8000": dict(k=19, N=8000, d=3, kernel=K_INV_R, scale=1.0, leaf=250, eta=float(np.sqrt(3.0)), s=1,
+                         eps=1e-6, pset=P_MIXED, nrhs=1, xdist="uniform_01", lo=-1.0, hi=1.0),
+    "3d_fig9_64000": dict(k=22, N=64000, d=3, kernel=K_INV_R, scale=1.0, leaf=250, eta=float(np.sqrt(3.0)), s=2,
+                          eps=1e-6, pset=P_MIXED, nrhs=1, xdist="uniform_01", lo=-1.0, hi=1.0),
+}
+FIG9_EPS = [1e-2, 1e-4, 1e-6, 1e-8, 1e-10]
