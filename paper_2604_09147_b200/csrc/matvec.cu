@@ -78,6 +78,9 @@ constexpr int THREADS = NCT + 32;      // + one producer warp
 #define HH_MV_PEEL2 0
 #endif
 constexpr int META = 64;
+#ifndef HH_MV_VEC1
+#define HH_MV_VEC1 1  // NR = 1 consumers with vector factor loads (0: the round-1 scalar consumers)
+#endif
 
 // FP64 tensor-core (DMMA m8n8k4) consumers for the multi-RHS contractions (NR = 8, 16):
 // the phase-1 tile is then D = W^T X (ct x NR) and the phase-2 leaf Y = U Z (nr x NR).
@@ -491,6 +494,147 @@ __device__ __forceinline__ void p1_mma_consumer(const P1Args &a, uint8_t *smem, 
   }
 }
 
+// ---- NR = 1 (the headline single-RHS product): vector factor loads.  At one RHS every stored
+// element costs a load, an exact up-conversion and a DFMA; loading V consecutive elements with
+// one 8/16-byte shared-memory access into V independent DFMA chains halves the issued
+// instructions per element (ncu r01: 13 thread-instructions per element, 61-68% issue-busy),
+// which keeps the kernels HBM-bound when the power cap lowers the SM clock.
+// V consecutive stored elements starting at e (aligned to V elements) -> fp64, exactly
+template <int TAG, int V>
+__device__ __forceinline__ void loadv(const typename Elem<TAG>::T *e, double (&w)[V]) {
+  if constexpr (V == 1) {
+    w[0] = up<TAG>(e[0]);
+  } else if constexpr (TAG == TAG_FP64) {
+#pragma unroll
+    for (int i = 0; i < V; i += 2) {
+      const double2 d = *reinterpret_cast<const double2 *>(e + i);
+      w[i] = d.x;
+      w[i + 1] = d.y;
+    }
+  } else if constexpr (TAG == TAG_FP32) {
+    if constexpr (V == 4) {
+      const float4 f = *reinterpret_cast<const float4 *>(e);
+      w[0] = f.x; w[1] = f.y; w[2] = f.z; w[3] = f.w;
+    } else {
+      const float2 f = *reinterpret_cast<const float2 *>(e);
+      w[0] = f.x; w[1] = f.y;
+    }
+  } else if constexpr (TAG == TAG_FP16 || TAG == TAG_BF16) {
+    uint32_t u[V / 2];
+    if constexpr (V == 4) {
+      const uint2 p = *reinterpret_cast<const uint2 *>(e);
+      u[0] = p.x; u[1] = p.y;
+    } else {
+      u[0] = *reinterpret_cast<const uint32_t *>(e);
+    }
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) {
+      if constexpr (TAG == TAG_FP16) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&u[i]));
+        w[2 * i] = f.x; w[2 * i + 1] = f.y;
+      } else {
+        w[2 * i] = (double)__uint_as_float(u[i] << 16);
+        w[2 * i + 1] = (double)__uint_as_float(u[i] & 0xFFFF0000u);
+      }
+    }
+  } else {  // q43
+    uint32_t u;
+    if constexpr (V == 4) u = *reinterpret_cast<const uint32_t *>(e);
+    else u = *reinterpret_cast<const uint16_t *>(e);
+#pragma unroll
+    for (int i = 0; i < V; ++i) w[i] = up<TAG_Q43>((uint8_t)(u >> (8 * i)));
+  }
+}
+
+// acc[i] += w(row j, element i) * v[j] over the cnt rows this thread owns (V chains)
+template <int TAG, int V>
+__device__ __forceinline__ void vec_acc(const typename Elem<TAG>::T *e, const double *v, int cnt, int es, int vs,
+                                        double (&acc)[4]) {
+#pragma unroll 2
+  for (int j = 0; j < cnt; ++j) {
+    double w[V];
+    loadv<TAG, V>(e, w);
+    const double x = *v;
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = __fma_rn(w[i], x, acc[i]);
+    e += es;
+    v += vs;
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void vec_acc_tag(int tag, const uint8_t *base, int e0, const double *v, int cnt, int es,
+                                            int vs, double (&acc)[4]) {
+  switch (tag) {
+    case TAG_FP64: vec_acc<TAG_FP64, V>(reinterpret_cast<const double *>(base) + e0, v, cnt, es, vs, acc); break;
+    case TAG_FP32: vec_acc<TAG_FP32, V>(reinterpret_cast<const float *>(base) + e0, v, cnt, es, vs, acc); break;
+    case TAG_FP16: vec_acc<TAG_FP16, V>(reinterpret_cast<const __half *>(base) + e0, v, cnt, es, vs, acc); break;
+    case TAG_BF16: vec_acc<TAG_BF16, V>(reinterpret_cast<const uint16_t *>(base) + e0, v, cnt, es, vs, acc); break;
+    default: vec_acc<TAG_Q43, V>(reinterpret_cast<const uint8_t *>(base) + e0, v, cnt, es, vs, acc); break;
+  }
+}
+
+// Phase-1 consumer at NR = 1: a tile whose width is a multiple of 4 is read as 4-column
+// vectors — thread = (column quad cq, row group q), 4 chains; narrower layouts keep one
+// column per thread.  The Q row groups of a column (quad) are adjacent lanes, reduced by
+// shuffles in a fixed order at the tile's last window.
+template <class G>
+__device__ __forceinline__ void p1_consumer_nr1(const P1Args &a, uint8_t *smem, uint64_t *full, uint64_t *empty,
+                                                int tid, int lane) {
+  int cur_ct = -1, V = 1, slots = 1, lq = 0, cs = 0, q = 0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int32_t zi[4] = {0, 0, 0, 0};
+  for (int n = 0;; ++n) {
+    const int s = n % G::STAGES;
+    mbar_wait(&full[s], (n / G::STAGES) & 1);
+    const uint8_t *st = smem + s * G::STAGE;
+    const Meta m = *reinterpret_cast<const Meta *>(st + G::WBUF + G::XBUF);
+    if (m.kind) break;
+    const int ct = m.a;
+    if (ct != cur_ct) {  // thread layout of this tile width (recomputed only when it changes)
+      cur_ct = ct;
+      V = (ct & 3) == 0 ? 4 : 1;
+      slots = ct / V;
+      lq = 0;  // Q = 2^lq row groups, <= 8, Q * slots <= NCT
+      while (lq < 3 && (2 << lq) * slots <= NCT) ++lq;
+      cs = tid >> lq;
+      q = tid & ((1 << lq) - 1);
+    }
+    const int Q = 1 << lq;
+    const bool active = cs < slots;
+    if (m.r0 == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i] = 0.0;
+        if (active && i < V && q == 0 && m.pb < 0) zi[i] = a.zmap[m.p + cs * V + i];
+      }
+    }
+    if (active) {
+      const uint8_t *wst = st + m.wlead;
+      const double *xst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
+      const int nrows = m.r1 - m.r0;
+      const int cnt = q < nrows ? (nrows - q + Q - 1) / Q : 0;
+      if (V == 4) vec_acc_tag<4>(m.b, wst, q * ct + 4 * cs, xst + q, cnt, Q * ct, Q, acc);
+      else vec_acc_tag<1>(m.b, wst, q * ct + cs, xst + q, cnt, Q * ct, Q, acc);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (m.r1 == m.q) {  // last window of the tile: fixed-order reduction over the Q row groups
+      for (int o = 1; o < Q; o <<= 1)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+      if (q == 0 && active) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < V) {
+            double *out = m.pb >= 0 ? a.partial + (m.pb + cs * V + i) : a.v + (a.N + zi[i]);
+            *out = acc[i];
+          }
+      }
+    }
+  }
+}
+
 template <int NR, int WP = 0>
 __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
   static_assert(WP == 0 || NR <= 4, "reduced working precision runs the FMA consumers (NR <= 4)");
@@ -563,6 +707,12 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
     p1_mma_consumer<NR, G>(a, smem, full, empty, warp, lane);
     return;
   }
+#if HH_MV_VEC1
+  if constexpr (WP == 0 && NR == 1) {
+    p1_consumer_nr1<G>(a, smem, full, empty, threadIdx.x, lane);
+    return;
+  }
+#endif
   // --------------------------------------------------------------------- consumers
   constexpr int MB = mblock<NR>();
   const int tid = threadIdx.x;
@@ -820,6 +970,70 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
   }
 }
 
+// Phase-2 consumer at NR = 1: thread = (row slot rs, column group g); a row slot is V = 4 (|R|
+// a multiple of 4), 2 (|R| even) or 1 consecutive rows of the leaf, read with one shared-memory
+// access per column (the U slab is column-major, so a slot's rows are adjacent and a warp reads
+// one contiguous span); V independent DFMA chains.  At the leaf's last window the Gn group
+// partials are summed in a fixed order through that stage's data area (held back from the
+// producer until the scatter y[perm[t]] (a10) is done).
+template <class G>
+__device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, uint64_t *full, uint64_t *empty,
+                                                int tid, int lane) {
+  static_assert(sizeof(double) * NCT * 4 <= (size_t)G::WBUF, "leaf reduction fits the stage");
+  int cur_nr = -1, V = 1, nslots = 1, Gn = 1, rs = 0, g = 0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int n = 0;; ++n) {
+    const int s = n % G::STAGES;
+    mbar_wait(&full[s], (n / G::STAGES) & 1);
+    uint8_t *st = smem + s * G::STAGE;
+    const Meta m = *reinterpret_cast<const Meta *>(st + G::WBUF + G::XBUF);
+    if (m.kind) break;
+    const int nr = m.a;
+    if (nr != cur_nr) {  // per-leaf layout (divisions only when the leaf size changes)
+      cur_nr = nr;
+      V = (nr & 3) == 0 ? 4 : (nr & 1) == 0 ? 2 : 1;
+      nslots = nr / V;
+      Gn = NCT / nslots;  // nr <= 256 (leaf_size limit)
+      rs = tid % nslots;
+      g = tid / nslots;
+    }
+    if (g < Gn) {
+      const uint8_t *ust = st + m.wlead;
+      const double *zst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
+      const int ncols = m.r1 - m.r0;
+      const int cnt = g < ncols ? (ncols - g + Gn - 1) / Gn : 0;
+      const int e0 = g * nr + rs * V;
+      if (V == 4) vec_acc_tag<4>(m.b & 0xff, ust, e0, zst + g, cnt, Gn * nr, Gn, acc);
+      else if (V == 2) vec_acc_tag<2>(m.b & 0xff, ust, e0, zst + g, cnt, Gn * nr, Gn, acc);
+      else vec_acc_tag<1>(m.b & 0xff, ust, e0, zst + g, cnt, Gn * nr, Gn, acc);
+    }
+    __syncwarp();
+    if (!(m.flags & 1)) {
+      if (lane == 0) mbar_arrive(&empty[s]);
+      continue;
+    }
+    // last window of the leaf: fixed-order reduction over the Gn groups in this stage's data
+    consumer_sync();  // every warp is done with the stage's U / z
+    double *red = reinterpret_cast<double *>(st);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      red[tid * 4 + i] = acc[i];
+      acc[i] = 0.0;
+    }
+    consumer_sync();
+    if (tid < nslots) {
+      for (int i = 0; i < V; ++i) {
+        double sum = 0.0;
+        for (int gg = 0; gg < Gn; ++gg) sum += red[(gg * nslots + tid) * 4 + i];
+        a.y[a.perm[m.p + tid * V + i]] = sum;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    consumer_sync();
+    if (lane == 0) mbar_arrive(&empty[s]);  // the stage goes back to the producer's TMA
+  }
+}
+
 template <int NR, int WP = 0>
 __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
   static_assert(WP == 0 || NR <= 4, "reduced working precision runs the FMA consumers (NR <= 4)");
@@ -896,6 +1110,12 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
     p2_mma_consumer<NR, G>(a, smem, full, empty, red, warp, lane);
     return;
   }
+#if HH_MV_VEC1
+  if constexpr (WP == 0 && NR == 1) {
+    p2_consumer_nr1<G>(a, smem, full, empty, threadIdx.x, lane);
+    return;
+  }
+#endif
   // --------------------------------------------------------------------- consumers
   constexpr int MB = mblock<NR>();
   const int tid = threadIdx.x;
