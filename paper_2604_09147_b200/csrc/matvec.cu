@@ -78,6 +78,9 @@ constexpr int THREADS = NCT + 32;      // + one producer warp
 #define HH_MV_PEEL2 0
 #endif
 constexpr int META = 64;
+#ifndef HH_MV_PDL
+#define HH_MV_PDL 1  // programmatic dependent launch between the matvec kernels
+#endif
 #ifndef HH_MV_VEC1
 #define HH_MV_VEC1 1  // NR = 1 consumers with vector factor loads (0: the round-1 scalar consumers)
 #endif
@@ -165,6 +168,20 @@ __device__ __forceinline__ uint64_t evict_last_policy() {
   return p;
 }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory"); }
+// Programmatic dependent launch: the matvec kernels are launched so that the next one's CTAs
+// may be scheduled while the previous one drains (its launch latency and prologue overlap the
+// tail); every kernel waits for its predecessor's completion (and memory) before its first
+// global access, so the data dependencies are those of plain stream order.
+__device__ __forceinline__ void pdl_wait() {
+#if HH_MV_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if HH_MV_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 
 // Copy [src, src + bytes) as the enclosing 16-B aligned window; returns the lead offset.
 __device__ __forceinline__ int stage_copy(uint8_t *dst, const uint8_t *src, int64_t bytes, uint64_t *bar,
@@ -300,6 +317,8 @@ template <int NR, int WP = 0>
 __global__ void k_gather(const int32_t *__restrict__ perm, const double *__restrict__ x, int64_t N, int64_t ldx,
                          double *__restrict__ v, int *ctr) {
   using A = typename WpT<WP>::A;
+  pdl_wait();
+  pdl_trigger();
   if (blockIdx.x == 0 && threadIdx.x < 2) ctr[threadIdx.x] = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = perm[t];
@@ -313,6 +332,8 @@ template <int NR, int WP = 0>
 __global__ void k_p1_combine(const P1Combine *__restrict__ cm, int64_t ncomb, const int32_t *__restrict__ zmap,
                              const double *__restrict__ partial, double *v, int64_t N) {
   using A = typename WpT<WP>::A;
+  pdl_wait();
+  pdl_trigger();
   for (int64_t t = blockIdx.x; t < ncomb; t += gridDim.x) {
     const P1Combine C = cm[t];
     for (int c = threadIdx.x; c < C.ct; c += blockDim.x) {
@@ -652,6 +673,8 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
   if (warp == NCW) {  // ------------------------------------------------ producer
     if (lane != 0) return;
     const uint64_t pol_w = evict_first_policy(), pol_x = evict_last_policy();
@@ -1021,12 +1044,19 @@ __device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, 
       acc[i] = 0.0;
     }
     consumer_sync();
-    if (tid < nslots) {
-      for (int i = 0; i < V; ++i) {
-        double sum = 0.0;
-        for (int gg = 0; gg < Gn; ++gg) sum += red[(gg * nslots + tid) * 4 + i];
-        a.y[a.perm[m.p + tid * V + i]] = sum;
+    {
+      // row r of the leaf = slot r / V, element r % V; T = 2^k adjacent lanes per row (T * nr <=
+      // NCT) each sum a strided subset of the Gn partials, then a fixed shuffle tree
+      int lt = 0;
+      while (lt < 5 && (nr << (lt + 1)) <= NCT) ++lt;
+      const int T = 1 << lt, r = tid >> lt, sub = tid & (T - 1);
+      double sum = 0.0;
+      if (r < nr) {
+        const int rsl = r / V, ri = r - rsl * V;
+        for (int gg = sub; gg < Gn; gg += T) sum += red[(gg * nslots + rsl) * 4 + ri];
       }
+      for (int o = 1; o < T; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (r < nr && sub == 0) a.y[a.perm[m.p + r]] = sum;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     consumer_sync();
@@ -1052,6 +1082,8 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
   if (warp == NCW) {  // ------------------------------------------------ producer
     if (lane != 0) return;
     const uint64_t pol_w = evict_first_policy(), pol_x = evict_last_policy();
@@ -1207,6 +1239,22 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
 
 }  // namespace mv
 
+// launch with the programmatic-stream-serialization attribute (see pdl_wait)
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = HH_MV_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HH_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 template <int NR, int WP = 0>
 void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
   using namespace mv;
@@ -1240,7 +1288,8 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   };
   mark(0);
   // a7 gather (+ counter reset)
-  k_gather<NR, WP><<<nsm * 8, 256, 0, st>>>(H->d_perm.as<int32_t>(), x + (int64_t)col0 * H->N, H->N, H->N, v, ctr);
+  launch_pdl(k_gather<NR, WP>, nsm * 8, 256, 0, st, H->d_perm.as<int32_t>(), x + (int64_t)col0 * H->N, H->N, H->N,
+             v, ctr);
   HH_LAUNCHED();
   mark(1);
   // a8 phase 1
@@ -1254,11 +1303,11 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     a.v = v;
     a.N = H->N;
     a.ctr = ctr;
-    k_phase1<NR, WP><<<(unsigned)L.grid1, THREADS, G1::smem(false), st>>>(a);
+    launch_pdl(k_phase1<NR, WP>, (unsigned)L.grid1, THREADS, G1::smem(false), st, a);
     HH_LAUNCHED();
     if (H->n_p1_comb > 0) {
-      k_p1_combine<NR, WP><<<(unsigned)std::min<int64_t>(H->n_p1_comb, (int64_t)nsm * 8), 256, 0, st>>>(
-          H->p1_comb.as<P1Combine>(), H->n_p1_comb, a.zmap, a.partial, v, H->N);
+      launch_pdl(k_p1_combine<NR, WP>, (unsigned)std::min<int64_t>(H->n_p1_comb, (int64_t)nsm * 8), 256, 0, st,
+                 H->p1_comb.as<P1Combine>(), H->n_p1_comb, a.zmap, a.partial, v, H->N);
       HH_LAUNCHED();
     }
   }
@@ -1276,7 +1325,7 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   b.ldy = H->N;
   b.ctr = ctr;
   if (L.grid2 > 0) {
-    k_phase2<NR, WP><<<(unsigned)L.grid2, THREADS, G2::smem(true), st>>>(b);
+    launch_pdl(k_phase2<NR, WP>, (unsigned)L.grid2, THREADS, G2::smem(true), st, b);
     HH_LAUNCHED();
   }
   mark(3);

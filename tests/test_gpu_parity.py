@@ -44,8 +44,11 @@ def test_check1b_ranks_and_tags(built):
     bad_r, bad_t, st = PL.rank_tag_parity(ex, Ho)
     print(name, st)
     assert bad_r == 0 and bad_t == 0, st
-    # ||H~||^2 agrees with the oracle's Alg. 4 value
-    assert abs(ex["info"]["norm2"] - Ho.norm2) <= 1e-12 * Ho.norm2
+    # ||H~||^2 agrees with the oracle's Alg. 4 value.  Tolerance (reading G26): the device's
+    # nb2_b = sum of the kept sigma^2 of Q^T A differs from the SVD's by at most the sketch
+    # residual R_b <= 1e-10 ||A_b||^2 it certifies, so the sum agrees to 1e-10 relative (2e-10
+    # with rounding); at eps = 1e-6 the sketches are wide and the agreement is ~1e-15
+    assert abs(ex["info"]["norm2"] - Ho.norm2) <= 2e-10 * Ho.norm2
 
 
 def test_check1c_packing_function(built):
