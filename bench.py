@@ -210,7 +210,7 @@ def stored_split(ex):
     sh = d * (L - B["level"].astype(np.int64))
     m = ls[(B["tgt"] + 1) << sh] - ls[B["tgt"] << sh]
     n = ls[(B["src"] + 1) << sh] - ls[B["src"] << sh]
-    wb = np.array([8, 4, 2, 2, 1])[B["tag"]]
+    wb = np.array([8, 4, 2, 2, 1, 3, 6])[B["tag"]]
     lr = B["storage"] == 0
     p = B["rank"].astype(np.int64)
     w_bytes = int(np.sum((p * n * wb)[lr]))
@@ -412,7 +412,8 @@ def run_ours(args, rank, world, local_rank):
                    "eps": cfg["eps"], "eta": cfg["eta"], "leaf_size": cfg["leaf"], "switch_level": cfg["s"],
                    "precision_set": cfg["pset"], "nrhs": nrhs, "parallelism": f"replicas{world}",
                    "stored_bytes": stored, "padded_bytes": info["padded_bytes"],
-                   "stored_bytes_by_tag": dict(zip(["fp64", "fp32", "fp16", "bf16", "q43", "dense_fp64"],
+                   "stored_bytes_by_tag": dict(zip(["fp64", "fp32", "fp16", "bf16", "q43", "bf24", "fp48",
+                                                    "dense_fp64"],
                                                    info["stored_bytes_tag"])),
                    "nblocks": info["nblocks"], "total_rank": info["total_rank"], "L": info["L"],
                    "l2_policy": "flush (2x L2 write) before each step" if flush else "inputs larger than L2",

@@ -68,12 +68,19 @@ typedef struct {
 } hh_kernel;
 
 /* precision_set bitmask (Table 1); FP64 (the working precision) is mandatory.
- * HH_P_Q43 (NEXT-3) adds Table 1's 8-bit q43 = (1-4-3), e_min -6, e_max 7, x_max 240, u = 2^-4
- * (reading G12), stored 1 byte per element with the OCP FP8 E4M3 encoding (identical for
- * |x| <= 240; the range guard promotes anything that rounds above 240). */
-enum { HH_P_FP64 = 1u, HH_P_FP32 = 2u, HH_P_FP16 = 4u, HH_P_BF16 = 8u, HH_P_Q43 = 16u };
+ * NEXT-3 opt-in formats:
+ *   HH_P_Q43  Table 1's 8-bit q43 = (1-4-3), e_min -6, e_max 7, x_max 240, u = 2^-4 (reading G12),
+ *             1 byte per element with the OCP FP8 E4M3 encoding (identical for |x| <= 240; the
+ *             range guard promotes anything that rounds above 240);
+ *   HH_P_BF24 / HH_P_FP48  the "memory accessor" continuum of PAPER.md:933 (§4.2 remark after
+ *             Eq. 4.4) at byte granularity: bf24 = (1-8-15), u = 2^-16, 3 bytes = the top 24 bits
+ *             of an fp32; fp48 = (1-11-36), u = 2^-37, 6 bytes = the top 48 bits of an fp64.
+ *             Stored by single RNE rounding, up-converted exactly (reading G28). */
+enum { HH_P_FP64 = 1u, HH_P_FP32 = 2u, HH_P_FP16 = 4u, HH_P_BF16 = 8u, HH_P_Q43 = 16u, HH_P_BF24 = 32u,
+       HH_P_FP48 = 64u, HH_P_ALL = 127u };
 /* tag ids used in exported tables */
-enum { HH_TAG_FP64 = 0, HH_TAG_FP32 = 1, HH_TAG_FP16 = 2, HH_TAG_BF16 = 3, HH_TAG_Q43 = 4, HH_NTAG = 5 };
+enum { HH_TAG_FP64 = 0, HH_TAG_FP32 = 1, HH_TAG_FP16 = 2, HH_TAG_BF16 = 3, HH_TAG_Q43 = 4, HH_TAG_BF24 = 5,
+       HH_TAG_FP48 = 6, HH_NTAG = 7 };
 /* OR into precision_set: compute ranks / tags / norms / byte ledger only, store no factors
  * (hh_matvec then returns HH_EINVAL).  Used for storage ratios of configurations that do
  * not fit in HBM (uniform-fp64 H_s at N = 2^20). */
@@ -196,11 +203,11 @@ typedef struct {
   int64_t n_lowrank, n_dense;
   int64_t total_rank;         /* sum of ranks = length of the z workspace */
   double norm2;               /* ||H~||_F^2 (Alg. 4) */
-  int64_t w_bytes[5];         /* W arena sizes per tag 0..4 (padded) */
-  int64_t u_bytes[5];         /* U arena sizes per tag 0..4 (padded) */
+  int64_t w_bytes[7];         /* W arena sizes per tag 0..6 (padded) */
+  int64_t u_bytes[7];         /* U arena sizes per tag 0..6 (padded) */
   int64_t d_bytes;            /* dense fp64 arena size (padded) */
   int64_t stored_bytes;       /* algorithmic: sum p(|I|+|J|) bytes(tag) + sum |I||J| 8 */
-  int64_t stored_bytes_tag[6];/* the same split by tag 0..4 and 5 = dense */
+  int64_t stored_bytes_tag[8];/* the same split by tag 0..6 and 7 = dense */
   int64_t padded_bytes;       /* bytes actually streamed by a matvec (arenas incl. padding) */
   int32_t c_far, c_nbr, c_sib;/* measured sparsity constants (max blocks per target) */
   int64_t n_fallback, n_promoted, n_coincident, n_retry;
@@ -230,7 +237,7 @@ typedef struct {
  * hh_export — copy tables and arena bytes to host memory.
  * Two-call protocol: call with every pointer NULL to get sizes via hh_info (or read
  * out->info); then set the pointers you want and call again.  Each pointer may be NULL
- * (skipped).  Arena windows: `arena` selects 0..4 = W[tag], 5..9 = U[tag], 10 = dense,
+ * (skipped).  Arena windows: `arena` selects 0..6 = W[tag], 7..13 = U[tag], 14 = dense,
  * bytes [arena_off, arena_off + arena_len) are copied to arena_dst.
  */
 typedef struct {
@@ -238,7 +245,7 @@ typedef struct {
   int32_t *perm;              /* [N]   tree position -> original index */
   int64_t *leaf_start;        /* [n_cells + 1] */
   hh_block_t *blocks;         /* [nblocks] */
-  int64_t *u_leaf_off;        /* [5 * (n_cells + 1)] byte offsets of leaf streams per tag */
+  int64_t *u_leaf_off;        /* [HH_NTAG * (n_cells + 1)] byte offsets of leaf streams per tag */
   int64_t *d_leaf_off;        /* [n_cells + 1] */
   int32_t arena;
   int64_t arena_off, arena_len;
@@ -253,7 +260,7 @@ hh_status hh_free(hh_handle H);
 /* Thread-local message for the last non-OK status on this thread ("" if none). */
 const char *hh_last_error(void);
 
-/* Test hook: the device storage-rounding routine of `tag` (HH_TAG_FP32/FP16/BF16/Q43) applied to
+/* Test hook: the device storage-rounding routine of `tag` (HH_TAG_FP32/FP16/BF16/Q43/BF24) applied to
  * n host doubles; host_bits receives the target bit patterns (RNE, single rounding, G16). */
 hh_status hh_selftest_round(const double *host_in, int64_t n, int32_t tag, uint32_t *host_bits);
 
@@ -264,8 +271,8 @@ hh_status hh_selftest_round(const double *host_in, int64_t n, int32_t tag, uint3
  *     `capacity` blocks (level, kind, tgt, src) and the total count to *nblocks (HH_EINVAL if
  *     capacity is too small: call with capacity 0 to size).
  *   hh_selftest_layout — the packing function (layout.cpp) for given blocks,
- *     ranks, tags and storage kinds: every offset hh_export reports, u_leaf_off[5*(ncell+1)],
- *     d_leaf_off[ncell+1] and w_bytes[5].
+ *     ranks, tags and storage kinds: every offset hh_export reports, u_leaf_off[HH_NTAG*(ncell+1)],
+ *     d_leaf_off[ncell+1] and w_bytes[HH_NTAG].
  */
 hh_status hh_selftest_partition(const int64_t *leaf_start, int32_t d, int32_t L, double eta, int32_t switch_level,
                                 int64_t capacity, int64_t *nblocks, uint8_t *level, uint8_t *kind, int64_t *tgt,

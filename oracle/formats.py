@@ -22,11 +22,12 @@ from __future__ import annotations
 
 import numpy as np
 
-FP64, FP32, FP16, BF16, Q43 = 0, 1, 2, 3, 4    # tag ids (same numbering as include/hh.h)
-TAGS = (FP64, FP32, FP16, BF16, Q43)
-TAG_NAMES = {FP64: "fp64", FP32: "fp32", FP16: "fp16", BF16: "bf16", Q43: "q43"}
-TAG_BIT = {FP64: 1, FP32: 2, FP16: 4, BF16: 8, Q43: 16}  # precision_set bitmask
-BYTES = {FP64: 8, FP32: 4, FP16: 2, BF16: 2, Q43: 1}
+FP64, FP32, FP16, BF16, Q43, BF24, FP48 = 0, 1, 2, 3, 4, 5, 6   # tag ids (as in include/hh.h)
+TAGS = (FP64, FP32, FP16, BF16, Q43, BF24, FP48)
+TAG_NAMES = {FP64: "fp64", FP32: "fp32", FP16: "fp16", BF16: "bf16", Q43: "q43", BF24: "bf24", FP48: "fp48"}
+TAG_BIT = {FP64: 1, FP32: 2, FP16: 4, BF16: 8, Q43: 16, BF24: 32, FP48: 64}  # precision_set bitmask
+ALL_FORMATS = 127
+BYTES = {FP64: 8, FP32: 4, FP16: 2, BF16: 2, Q43: 1, BF24: 3, FP48: 6}
 BITS = {t: 8 * b for t, b in BYTES.items()}
 
 # (mantissa bits m, e_min, e_max) — Table 1 columns (1-e-m), e_min, e_max
@@ -36,7 +37,16 @@ PARAMS = {
     FP16: (10, -14, 15),
     BF16: (7, -126, 127),
     Q43: (3, -6, 7),
+    # PAPER.md:933 (remark after Eq. 4.4): "by leveraging memory accessor mechanisms, one can
+    # exploit a continuum of precision formats for storing data ... with exactly the right number
+    # of bits".  Reading G28: at byte granularity, between the Table 1 formats — bf24 keeps fp32's
+    # exponent range with a 15-bit mantissa (3 bytes), fp48 fp64's range with a 36-bit mantissa
+    # (6 bytes): the top bytes of the wider IEEE pattern.
+    BF24: (15, -126, 127),
+    FP48: (36, -1022, 1023),
 }
+# formats in decreasing unit roundoff (Eq. 4.4 picks the largest admissible u)
+BY_U = tuple(sorted(TAGS, key=lambda t: PARAMS[t][0]))
 
 
 def unit_roundoff(tag: int) -> float:
@@ -95,6 +105,12 @@ def to_storage_bits(x64, tag: int) -> np.ndarray:
     if tag == BF16:
         f32 = r.astype(np.float32).view(np.uint32)
         return (f32 >> np.uint32(16)).astype(np.uint16)
+    if tag == BF24:   # the top 3 bytes of the (exact) fp32 pattern, little-endian
+        f32 = r.astype(np.float32).view(np.uint32) >> np.uint32(8)
+        return np.stack([(f32 >> np.uint32(8 * k)) & np.uint32(0xFF) for k in range(3)], axis=-1).astype(np.uint8)
+    if tag == FP48:   # the top 6 bytes of the fp64 pattern, little-endian
+        f64 = r.view(np.uint64) >> np.uint64(16)
+        return np.stack([(f64 >> np.uint64(8 * k)) & np.uint64(0xFF) for k in range(6)], axis=-1).astype(np.uint8)
     # q43 (1-4-3, bias 7): sign | exponent field | 3 mantissa bits, from the exact rounded value
     a = np.abs(r)
     sign = (np.signbit(r)).astype(np.uint8) << np.uint8(7)
@@ -123,6 +139,16 @@ def from_storage_bytes(buf: bytes | np.ndarray, tag: int) -> np.ndarray:
     if tag == BF16:
         hi = b.view("<u2").astype(np.uint32) << np.uint32(16)
         return hi.view(np.float32).astype(np.float64)
+    if tag == BF24:
+        t = b.reshape(-1, 3).astype(np.uint32)
+        bits = (t[:, 0] << np.uint32(8)) | (t[:, 1] << np.uint32(16)) | (t[:, 2] << np.uint32(24))
+        return bits.view(np.float32).astype(np.float64)
+    if tag == FP48:
+        t = b.reshape(-1, 6).astype(np.uint64)
+        bits = np.zeros(t.shape[0], np.uint64)
+        for k in range(6):
+            bits |= t[:, k] << np.uint64(8 * (k + 2))
+        return bits.view(np.float64).copy()
     # q43: (-1)^s (1 + m/8) 2^(e-7) for exponent field e in 1..14, (-1)^s (m/8) 2^-6 for e = 0
     e = ((b >> 3) & 0xF).astype(np.int64)
     m = (b & 0x7).astype(np.float64)

@@ -36,7 +36,7 @@ TIE_FP16 = 1 << 17   # precision_set flag (include/hh.h HH_TIE_FP16): fp16 over 
 def choose_tag(nb2: float, norm2: float, eps: float, d: int, l: int, pset: int) -> tuple[int, bool]:
     """Eq. 4.4 / Alg. 2 line 4: largest admissible unit roundoff (squared, exact form)."""
     rhs = (eps * eps) * norm2
-    for tag in (F.Q43, F.BF16, F.FP16, F.FP32, F.FP64):   # decreasing unit roundoff
+    for tag in F.BY_U:                                    # decreasing unit roundoff
         if not (pset & F.TAG_BIT[tag]):
             continue
         u = F.unit_roundoff(tag)
@@ -47,7 +47,7 @@ def choose_tag(nb2: float, norm2: float, eps: float, d: int, l: int, pset: int) 
 
 def guard_tag(tag: int, maxabs: float, pset: int) -> tuple[int, bool]:
     """Range guard: while rounding the largest factor entry to `tag` overflows, promote."""
-    order = [t for t in (F.Q43, F.BF16, F.FP16, F.FP32, F.FP64) if pset & F.TAG_BIT[t]]
+    order = [t for t in F.BY_U if pset & F.TAG_BIT[t]]
     promoted = False
     i = order.index(tag)
     while np.isinf(F.round_rne(np.array([maxabs]), order[i])[0]) and order[i] != F.FP64:
@@ -76,7 +76,7 @@ def tag_blocks(d, level, kind, m, n, rank, nb2, tot, maxabs, eps, pset) -> dict:
     pre-rule rank and tag of every low-rank candidate (lr_rank, lr_tag), ||H~||^2, the
     fallback / promoted counts and each tag decision's relative distance from its threshold."""
     nb = len(kind)
-    mixed = (pset & 0x1F) != F.TAG_BIT[F.FP64]
+    mixed = (pset & F.ALL_FORMATS) != F.TAG_BIT[F.FP64]
     norm2 = alg4_norm2(kind, nb2, tot)
     tag = np.zeros(nb, np.int64)
     lr_tag = np.full(nb, -1, np.int64)
@@ -98,7 +98,7 @@ def tag_blocks(d, level, kind, m, n, rank, nb2, tot, maxabs, eps, pset) -> dict:
         lhs = (u * u) * 2.0 ** (d * l) * float(nb2[b])
         tm = (rhs - lhs) / rhs if rhs else np.inf
         if t != F.Q43:   # also distance to qualifying for the next larger u
-            nxt = [c for c in (F.FP32, F.FP16, F.BF16, F.Q43) if F.unit_roundoff(c) > u and (pset & F.TAG_BIT[c])]
+            nxt = [c for c in F.TAGS if F.unit_roundoff(c) > u and (pset & F.TAG_BIT[c])]
             if nxt:
                 un = min(F.unit_roundoff(c) for c in nxt)
                 tm = min(abs(tm), abs(((un * un) * 2.0 ** (d * l) * float(nb2[b]) - rhs) / rhs))
@@ -177,7 +177,7 @@ def build(P, kernel, scale, eps, eta, leaf, s, pset, keep_exact=False) -> Oracle
     H.margin = np.full(nb, np.inf)
     H.maxabs_w = np.zeros(nb)
     H.tag_margin = np.full(nb, np.inf)
-    mixed = (pset & 0x1F) != F.TAG_BIT[F.FP64]  # format bits only (flags such as TIE_FP16 excluded)
+    mixed = (pset & F.ALL_FORMATS) != F.TAG_BIT[F.FP64]  # format bits only (flags such as TIE_FP16 excluded)
     perm = tree.perm
     exact = {}
     # Alg. 1 + Alg. 4: compress every admissible block, norms from singular values

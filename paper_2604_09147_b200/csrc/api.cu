@@ -29,6 +29,7 @@ __global__ void k_round(const double *in, int64_t n, int tag, uint32_t *out) {
   out[i] = tag == TAG_FP32   ? to_fp32_bits(in[i])
            : tag == TAG_FP16 ? to_fp16_bits(in[i])
            : tag == TAG_BF16 ? to_bf16_bits(in[i])
+           : tag == TAG_BF24 ? to_bf24_bits(in[i])
                              : to_q43_bits(in[i]);
 }
 
@@ -158,7 +159,7 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
   if (leaf_size < 1) return fail(HH_EINVAL, "leaf_size must be >= 1");
   if (leaf_size > 256) return fail(HH_EUNSUPPORTED, "leaf_size > 256 not supported by this build");
   if (!(precision_set & HH_P_FP64)) return fail(HH_EINVAL, "precision_set must contain HH_P_FP64");
-  if (precision_set & ~(0x1Fu | HH_LEDGER_ONLY | HH_TIE_FP16)) return fail(HH_EINVAL, "unknown precision_set bits");
+  if (precision_set & ~(HH_P_ALL | HH_LEDGER_ONLY | HH_TIE_FP16)) return fail(HH_EINVAL, "unknown precision_set bits");
   if (kernel.kind < 0 || kernel.kind > 4) return fail(HH_EINVAL, "unknown kernel kind");
   if ((kernel.kind == HH_K_GAUSS || kernel.kind == HH_K_EXP) && !(kernel.scale > 0.0))
     return fail(HH_EINVAL, "kernel scale must be > 0");
@@ -177,7 +178,7 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
     H->eta = eta;
     H->leaf_size = leaf_size;
     H->s = switch_level;
-    H->pset = precision_set & 0x1F;
+    H->pset = precision_set & HH_P_ALL;
     H->ledger = (precision_set & HH_LEDGER_ONLY) != 0;
     H->tie16 = (precision_set & HH_TIE_FP16) && (precision_set & HH_P_FP16) && (precision_set & HH_P_BF16);
     DBuf pts;
@@ -467,7 +468,7 @@ hh_status hh_export(hh_handle H, hh_export_t *out) {
       if (out->arena >= 0 && out->arena < NTAG) src = &H->W[out->arena];
       else if (out->arena >= NTAG && out->arena < 2 * NTAG) src = &H->U[out->arena - NTAG];
       else if (out->arena == 2 * NTAG) src = &H->D;
-      if (!src) return fail(HH_EINVAL, "arena must be 0..10");
+      if (!src) return fail(HH_EINVAL, "arena must be 0 .. 2 * HH_NTAG");
       const int64_t size = out->arena < NTAG       ? H->w_bytes[out->arena]
                            : out->arena < 2 * NTAG ? H->u_bytes[out->arena - NTAG]
                                                    : H->d_bytes;
@@ -491,7 +492,7 @@ hh_status hh_switch_level_search(const double *points, int64_t N, int32_t d, hh_
                                  int32_t *out_level, int32_t *out_L, int64_t *bytes, int32_t bytes_len) {
   g_err.clear();
   if (!out_level) return fail(HH_EINVAL, "NULL pointer");
-  const uint32_t pset = (precision_set & (0x1Fu | HH_TIE_FP16)) | HH_LEDGER_ONLY;
+  const uint32_t pset = (precision_set & (HH_P_ALL | HH_TIE_FP16)) | HH_LEDGER_ONLY;
   auto ledger_bytes = [&](int32_t s, int64_t &out, int32_t *L) -> hh_status {
     hh_handle h = nullptr;
     const hh_status st = hh_build(points, N, d, kernel, eps, eta, leaf_size, s, pset, cuda_stream, &h);
@@ -620,7 +621,7 @@ hh_status hh_selftest_tags(const int64_t *leaf_start, int32_t d, int32_t L, int6
     H.eps = eps;
     H.ncell = 1ll << (d * L);
     H.leaf_start.assign(leaf_start, leaf_start + H.ncell + 1);
-    H.pset = precision_set & 0x1F;
+    H.pset = precision_set & HH_P_ALL;
     H.tie16 = (precision_set & HH_TIE_FP16) && (precision_set & HH_P_FP16) && (precision_set & HH_P_BF16);
     H.level.assign(level, level + nblocks);
     H.kind.assign(kind, kind + nblocks);
@@ -656,7 +657,7 @@ hh_status hh_selftest_tags(const int64_t *leaf_start, int32_t d, int32_t L, int6
  * return the bit patterns (checked against the oracle's definition-based rounding). */
 hh_status hh_selftest_round(const double *host_in, int64_t n, int32_t tag, uint32_t *host_bits) {
   g_err.clear();
-  if (!host_in || !host_bits || n < 0 || tag < 1 || tag > 4) return fail(HH_EINVAL, "bad argument");
+  if (!host_in || !host_bits || n < 0 || tag < 1 || tag > 5) return fail(HH_EINVAL, "bad argument");
   try {
     DBuf a, b;
     a.alloc(sizeof(double) * n);

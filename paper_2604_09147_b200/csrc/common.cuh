@@ -46,12 +46,14 @@ void count_launch(int n = 1);  // launch accounting (api.cpp)
   } while (0)
 
 // ------------------------------------------------------------------ constants
-constexpr int TAG_FP64 = 0, TAG_FP32 = 1, TAG_FP16 = 2, TAG_BF16 = 3, TAG_Q43 = 4;
-constexpr int NTAG = 5;
+constexpr int TAG_FP64 = 0, TAG_FP32 = 1, TAG_FP16 = 2, TAG_BF16 = 3, TAG_Q43 = 4, TAG_BF24 = 5, TAG_FP48 = 6;
+constexpr int NTAG = 7;
 constexpr int KIND_FAR = 0, KIND_NBR = 1, KIND_SIB = 2, KIND_LNBR = 3, KIND_DIAG = 4;
 constexpr int STORE_LR = 0, STORE_DENSE = 1;
 constexpr int64_t ALIGN = 16;
-__host__ __device__ inline int tag_bytes(int t) { return t == TAG_FP64 ? 8 : t == TAG_FP32 ? 4 : t == TAG_Q43 ? 1 : 2; }
+__host__ __device__ inline int tag_bytes(int t) {
+  return t == TAG_FP64 ? 8 : t == TAG_FP32 ? 4 : t == TAG_Q43 ? 1 : t == TAG_BF24 ? 3 : t == TAG_FP48 ? 6 : 2;
+}
 inline int64_t align_up(int64_t x, int64_t a = ALIGN) { return (x + a - 1) / a * a; }
 
 // ------------------------------------------------------------------ kernel functions
@@ -131,5 +133,18 @@ __host__ __device__ inline uint16_t to_bf16_bits(double x) { return (uint16_t)rn
 __host__ __device__ inline uint32_t to_fp32_bits(double x) { return rne_bits<23, -126, 127>(x); }
 // q43 (Table 1: 1-4-3, e_min -6, e_max 7): exponent field 15 = inf, x_max = 240
 __host__ __device__ inline uint8_t to_q43_bits(double x) { return (uint8_t)rne_bits<3, -6, 7>(x); }
+// accessor formats: bf24 = 1-8-15 (fp32's range, the top 24 bits of an fp32)
+__host__ __device__ inline uint32_t to_bf24_bits(double x) { return rne_bits<15, -126, 127>(x); }
+// fp48 = 1-11-36 (fp64's range, the top 48 bits of an fp64): RNE at bit 16 of the fp64 pattern
+// (normals and subnormals alike: a 1-11-36 subnormal has spacing 2^(-1022-36) = 2^16 fp64
+// subnormal ulps); a carry into the exponent field is the correct rounding, inf stays inf
+__host__ __device__ inline uint64_t to_fp48_bits(double x) {
+  uint64_t b;
+  memcpy(&b, &x, 8);
+  const uint64_t mag = b & 0x7FFFFFFFFFFFFFFFull;
+  if (mag >= 0x7FF0000000000000ull) return b >> 16;  // inf / nan
+  const uint64_t r = mag + 0x7FFFull + ((mag >> 16) & 1ull);
+  return ((b & 0x8000000000000000ull) | (r & 0xFFFFFFFFFFFF0000ull)) >> 16;
+}
 
 }  // namespace hh

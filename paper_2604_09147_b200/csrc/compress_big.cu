@@ -139,7 +139,21 @@ __device__ __forceinline__ void store_tag(uint8_t *base, int64_t elem, int tag, 
     case TAG_FP32: reinterpret_cast<uint32_t *>(base)[elem] = to_fp32_bits(v); break;
     case TAG_FP16: reinterpret_cast<uint16_t *>(base)[elem] = to_fp16_bits(v); break;
     case TAG_BF16: reinterpret_cast<uint16_t *>(base)[elem] = to_bf16_bits(v); break;
-    default: base[elem] = to_q43_bits(v);
+    case TAG_Q43: base[elem] = to_q43_bits(v); break;
+    case TAG_BF24: {
+      const uint32_t b = to_bf24_bits(v);
+      base[3 * elem] = (uint8_t)b;
+      base[3 * elem + 1] = (uint8_t)(b >> 8);
+      base[3 * elem + 2] = (uint8_t)(b >> 16);
+      break;
+    }
+    default: {  // fp48
+      const uint64_t b = to_fp48_bits(v);
+      uint16_t *h = reinterpret_cast<uint16_t *>(base) + 3 * elem;
+      h[0] = (uint16_t)b;
+      h[1] = (uint16_t)(b >> 16);
+      h[2] = (uint16_t)(b >> 32);
+    }
   }
 }
 

@@ -66,7 +66,7 @@ struct P2Seg {
   int64_t src;        // byte offset of column 0 in U[tag] (or D); multiple of the element size
   int64_t vbeg;       // v index of column 0's vector entry (z for U, x~ for dense)
   int32_t ncols;
-  int16_t tag;        // 0..4 (dense: 0)
+  int16_t tag;        // 0..NTAG-1 (dense: 0)
   int16_t dense;      // 1 -> dense arena
 };
 struct P2Leaf {
@@ -104,7 +104,7 @@ struct hh_matrix {
   int64_t ztotal = 0;
   // arenas
   hh::DBuf W[hh::NTAG], U[hh::NTAG], D;
-  int64_t w_bytes[hh::NTAG] = {0, 0, 0, 0, 0}, u_bytes[hh::NTAG] = {0, 0, 0, 0, 0}, d_bytes = 0;
+  int64_t w_bytes[hh::NTAG] = {}, u_bytes[hh::NTAG] = {}, d_bytes = 0;
   // matvec plan
   hh::DBuf p1_tiles, zmap, p2_segs, p2_leaves, p1_comb, partial;
   int64_t n_p1_tiles = 0, n_p2_leaves = 0, n_p1_comb = 0, n_partial = 0;

@@ -19,10 +19,10 @@
 
 namespace hh {
 
-static const double kU[NTAG] = {0x1p-53, 0x1p-24, 0x1p-11, 0x1p-8, 0x1p-4};
-static const uint32_t kBit[NTAG] = {HH_P_FP64, HH_P_FP32, HH_P_FP16, HH_P_BF16, HH_P_Q43};
+static const double kU[NTAG] = {0x1p-53, 0x1p-24, 0x1p-11, 0x1p-8, 0x1p-4, 0x1p-16, 0x1p-37};
+static const uint32_t kBit[NTAG] = {HH_P_FP64, HH_P_FP32, HH_P_FP16, HH_P_BF16, HH_P_Q43, HH_P_BF24, HH_P_FP48};
 // formats in decreasing unit roundoff (the order Eq. 4.4 tries them; the range guard steps right)
-static const int kByU[NTAG] = {TAG_Q43, TAG_BF16, TAG_FP16, TAG_FP32, TAG_FP64};
+static const int kByU[NTAG] = {TAG_Q43, TAG_BF16, TAG_FP16, TAG_BF24, TAG_FP32, TAG_FP48, TAG_FP64};
 
 void cluster_range(const hh_matrix *H, int l, int64_t m, int64_t &a, int64_t &n) {
   const int sh = H->d * (H->L - l);
@@ -38,13 +38,15 @@ static bool overflows(int tag, double x) {
     case TAG_FP16: return (to_fp16_bits(x) & 0x7FFFu) == 0x7C00u;
     case TAG_BF16: return (to_bf16_bits(x) & 0x7FFFu) == 0x7F80u;
     case TAG_Q43: return (to_q43_bits(x) & 0x7Fu) == 0x78u;
+    case TAG_BF24: return (to_bf24_bits(x) & 0x7FFFFFu) == 0x7F8000u;
+    case TAG_FP48: return (to_fp48_bits(x) & 0x7FFFFFFFFFFFull) == 0x7FF000000000ull;
     default: return false;
   }
 }
 
 void assign_tags(hh_matrix *H) {
   const size_t nb = H->level.size();
-  const bool mixed = (H->pset & 0x1F) != HH_P_FP64;
+  const bool mixed = (H->pset & HH_P_ALL) != HH_P_FP64;
   // a4: global norm in canonical order
   double norm2 = 0.0;
   for (size_t b = 0; b < nb; ++b) {
@@ -149,7 +151,7 @@ void compute_layout(hh_matrix *H) {
       if (H->src[a] != H->src[c]) return H->src[a] < H->src[c];
       return H->tgt[a] < H->tgt[c];
     });
-    int64_t off[NTAG] = {0, 0, 0, 0, 0};
+    int64_t off[NTAG] = {};
     size_t i = 0;
     while (i < idx.size()) {
       size_t e = i;
@@ -194,7 +196,7 @@ void compute_layout(hh_matrix *H) {
     while (b < nb) {
       size_t e = b;
       while (e < nb && H->level[e] == H->level[b] && H->tgt[e] == H->tgt[b]) ++e;
-      int64_t within[NTAG] = {0, 0, 0, 0, 0};
+      int64_t within[NTAG] = {};
       for (size_t i = b; i < e; ++i)
         if (is_lr(i) && H->rank[i] > 0) {
           const int g = H->tag[i];
@@ -237,7 +239,7 @@ void compute_layout(hh_matrix *H) {
       }
   }
   // ledger
-  int64_t tagged[NTAG + 1] = {0, 0, 0, 0, 0, 0};
+  int64_t tagged[NTAG + 1] = {};
   int64_t nlr = 0, nd = 0;
   for (size_t b = 0; b < nb; ++b) {
     if (H->storage[b] == STORE_DENSE) {

@@ -195,7 +195,7 @@ __device__ __forceinline__ int stage_copy(uint8_t *dst, const uint8_t *src, int6
 }
 // arena base by tag without dynamic indexing of the kernel-parameter array (no local memory)
 __device__ __forceinline__ const uint8_t *pick(const uint8_t *const (&arr)[NTAG], int t) {
-  return t == 0 ? arr[0] : t == 1 ? arr[1] : t == 2 ? arr[2] : t == 3 ? arr[3] : arr[4];
+  return t == 0 ? arr[0] : t == 1 ? arr[1] : t == 2 ? arr[2] : t == 3 ? arr[3] : t == 4 ? arr[4] : t == 5 ? arr[5] : arr[6];
 }
 __device__ __forceinline__ uint32_t window_bytes(const uint8_t *src, int64_t bytes) {
   const uintptr_t s = (uintptr_t)src;
@@ -208,6 +208,26 @@ template <> struct Elem<TAG_FP32> { using T = float; };
 template <> struct Elem<TAG_FP16> { using T = __half; };
 template <> struct Elem<TAG_BF16> { using T = uint16_t; };
 template <> struct Elem<TAG_Q43> { using T = uint8_t; };
+// accessor formats (NEXT-3): the top 3 bytes of an fp32 / top 6 bytes of an fp64
+struct B24 { uint8_t b[3]; };
+struct B48 { uint16_t h[3]; };
+static_assert(sizeof(B24) == 3 && sizeof(B48) == 6, "packed accessor elements");
+template <> struct Elem<TAG_BF24> { using T = B24; };
+template <> struct Elem<TAG_FP48> { using T = B48; };
+
+// f(std::integral_constant<int, TAG>) for the runtime tag (one branch per storage format)
+template <class F>
+__device__ __forceinline__ void dispatch_tag(int tag, F &&f) {
+  switch (tag) {
+    case TAG_FP64: f(std::integral_constant<int, TAG_FP64>{}); break;
+    case TAG_FP32: f(std::integral_constant<int, TAG_FP32>{}); break;
+    case TAG_FP16: f(std::integral_constant<int, TAG_FP16>{}); break;
+    case TAG_BF16: f(std::integral_constant<int, TAG_BF16>{}); break;
+    case TAG_Q43: f(std::integral_constant<int, TAG_Q43>{}); break;
+    case TAG_BF24: f(std::integral_constant<int, TAG_BF24>{}); break;
+    default: f(std::integral_constant<int, TAG_FP48>{}); break;
+  }
+}
 
 // Tunables (compile-time; scripts/variants.sh builds alternatives side by side).
 #ifndef HH_MV_CVT
@@ -219,6 +239,12 @@ template <int TAG>
 __device__ __forceinline__ double up(const typename Elem<TAG>::T v) {
   if constexpr (TAG == TAG_FP64) {
     return v;
+  } else if constexpr (TAG == TAG_BF24) {  // 1-8-15: the bytes are the top 24 bits of an fp32
+    const uint32_t b = (uint32_t)v.b[0] | ((uint32_t)v.b[1] << 8) | ((uint32_t)v.b[2] << 16);
+    return (double)__uint_as_float(b << 8);
+  } else if constexpr (TAG == TAG_FP48) {  // 1-11-36: the top 48 bits of an fp64
+    const uint64_t b = (uint64_t)v.h[0] | ((uint64_t)v.h[1] << 16) | ((uint64_t)v.h[2] << 32);
+    return __longlong_as_double((long long)(b << 16));
   } else if constexpr (TAG == TAG_Q43) {
     // q43 byte s|eeee|mmm (bias 7) placed in an fp16's top bits (exponent field 0eeee, mantissa
     // mmm0000000) is the same value scaled by 2^-8, normals and subnormals alike: exact
@@ -298,12 +324,15 @@ template <int TAG, class A> __device__ __forceinline__ A wp_elem(const typename 
     else if constexpr (TAG == TAG_FP32) return v;
     else if constexpr (TAG == TAG_FP16) return __half2float(v);
     else if constexpr (TAG == TAG_BF16) return __uint_as_float(((uint32_t)v) << 16);
-    else return (float)up<TAG_Q43>(v);
+    else if constexpr (TAG == TAG_FP48) return __double2float_rn(up<TAG>(v));
+    else return (float)up<TAG>(v);  // q43, bf24: exact in fp32
   } else {
     if constexpr (TAG == TAG_FP64) return __double2half(v);
     else if constexpr (TAG == TAG_FP32) return __float2half_rn(v);
     else if constexpr (TAG == TAG_FP16) return v;
     else if constexpr (TAG == TAG_BF16) return __float2half_rn(__uint_as_float(((uint32_t)v) << 16));
+    else if constexpr (TAG == TAG_BF24) return __float2half_rn((float)up<TAG>(v));
+    else if constexpr (TAG == TAG_FP48) return __double2half(up<TAG>(v));
     else {
       const uint32_t b = v;  // q43 values are exact in fp16: bit placement then x 2^8
       return __hmul(__ushort_as_half((unsigned short)(((b & 0x80u) << 8) | ((b & 0x7Fu) << 7))),
@@ -490,13 +519,7 @@ __device__ __forceinline__ void p1_mma_consumer(const P1Args &a, uint8_t *smem, 
       const uint8_t *wst = st + m.wlead;
       const double *xst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
       const int nrows = m.r1 - m.r0;
-      switch (m.b) {
-        case TAG_FP64: p1_mma_rows<TAG_FP64, NR>(wst, xst, nrows, ct, col0, lane, c); break;
-        case TAG_FP32: p1_mma_rows<TAG_FP32, NR>(wst, xst, nrows, ct, col0, lane, c); break;
-        case TAG_FP16: p1_mma_rows<TAG_FP16, NR>(wst, xst, nrows, ct, col0, lane, c); break;
-        case TAG_BF16: p1_mma_rows<TAG_BF16, NR>(wst, xst, nrows, ct, col0, lane, c); break;
-        default: p1_mma_rows<TAG_Q43, NR>(wst, xst, nrows, ct, col0, lane, c); break;
-      }
+      dispatch_tag(m.b, [&](auto t) { p1_mma_rows<decltype(t)::value, NR>(wst, xst, nrows, ct, col0, lane, c); });
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -558,6 +581,36 @@ __device__ __forceinline__ void loadv(const typename Elem<TAG>::T *e, double (&w
         w[2 * i + 1] = (double)__uint_as_float(u[i] & 0xFFFF0000u);
       }
     }
+  } else if constexpr (TAG == TAG_BF24) {
+    // V elements = 3V bytes, 4-byte (V = 4) / 2-byte (V = 2) aligned: whole words, then shifts
+    if constexpr (V == 4) {
+      const uint32_t *p = reinterpret_cast<const uint32_t *>(e);
+      const uint32_t a = p[0], b = p[1], c = p[2];
+      w[0] = (double)__uint_as_float(a << 8);
+      w[1] = (double)__uint_as_float(__funnelshift_l(a, b, 16) & 0xFFFFFF00u);  // bytes 3..5
+      w[2] = (double)__uint_as_float(__funnelshift_l(b, c, 24) & 0xFFFFFF00u);  // bytes 6..8
+      w[3] = (double)__uint_as_float(c & 0xFFFFFF00u);
+    } else {
+      const uint16_t *p = reinterpret_cast<const uint16_t *>(e);
+      const uint32_t a = p[0], b = p[1], c = p[2];  // bytes 0..5
+      w[0] = (double)__uint_as_float((a << 8) | (b << 24));
+      w[1] = (double)__uint_as_float((b & 0xFF00u) | (c << 16));
+    }
+  } else if constexpr (TAG == TAG_FP48) {
+    // V elements = 6V bytes, 8-byte (V = 4) / 4-byte (V = 2) aligned
+    if constexpr (V == 4) {
+      const uint64_t *p = reinterpret_cast<const uint64_t *>(e);
+      const uint64_t a = p[0], b = p[1], c = p[2];
+      w[0] = __longlong_as_double((long long)(a << 16));
+      w[1] = __longlong_as_double((long long)(((a >> 48) | (b << 16)) << 16));
+      w[2] = __longlong_as_double((long long)((((b >> 32) | (c << 32)) << 16)));
+      w[3] = __longlong_as_double((long long)(c & 0xFFFFFFFFFFFF0000ull));
+    } else {
+      const uint32_t *p = reinterpret_cast<const uint32_t *>(e);
+      const uint64_t a = p[0], b = p[1], c = p[2];  // bytes 0..11
+      w[0] = __longlong_as_double((long long)(((a | (b << 32)) << 16)));
+      w[1] = __longlong_as_double((long long)((((b >> 16) | (c << 16)) << 16)));
+    }
   } else {  // q43
     uint32_t u;
     if constexpr (V == 4) u = *reinterpret_cast<const uint32_t *>(e);
@@ -586,13 +639,10 @@ __device__ __forceinline__ void vec_acc(const typename Elem<TAG>::T *e, const do
 template <int V>
 __device__ __forceinline__ void vec_acc_tag(int tag, const uint8_t *base, int e0, const double *v, int cnt, int es,
                                             int vs, double (&acc)[4]) {
-  switch (tag) {
-    case TAG_FP64: vec_acc<TAG_FP64, V>(reinterpret_cast<const double *>(base) + e0, v, cnt, es, vs, acc); break;
-    case TAG_FP32: vec_acc<TAG_FP32, V>(reinterpret_cast<const float *>(base) + e0, v, cnt, es, vs, acc); break;
-    case TAG_FP16: vec_acc<TAG_FP16, V>(reinterpret_cast<const __half *>(base) + e0, v, cnt, es, vs, acc); break;
-    case TAG_BF16: vec_acc<TAG_BF16, V>(reinterpret_cast<const uint16_t *>(base) + e0, v, cnt, es, vs, acc); break;
-    default: vec_acc<TAG_Q43, V>(reinterpret_cast<const uint8_t *>(base) + e0, v, cnt, es, vs, acc); break;
-  }
+  dispatch_tag(tag, [&](auto t) {
+    constexpr int TG = decltype(t)::value;
+    vec_acc<TG, V>(reinterpret_cast<const typename Elem<TG>::T *>(base) + e0, v, cnt, es, vs, acc);
+  });
 }
 
 // Phase-1 consumer at NR = 1: a tile whose width is a multiple of 4 is read as 4-column
@@ -776,28 +826,11 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
       const int nrows = m.r1 - m.r0;
       const int cnt = q < nrows ? (nrows - q + Q - 1) / Q : 0;
       const int e0 = q * ct + cs;
-      switch (m.b) {
-        case TAG_FP64:
-          block_acc<TAG_FP64, NR, MB, A>(reinterpret_cast<const double *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
-                                      Q * NR, valid, acc);
-          break;
-        case TAG_FP32:
-          block_acc<TAG_FP32, NR, MB, A>(reinterpret_cast<const float *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
-                                      Q * NR, valid, acc);
-          break;
-        case TAG_FP16:
-          block_acc<TAG_FP16, NR, MB, A>(reinterpret_cast<const __half *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
-                                      Q * NR, valid, acc);
-          break;
-        case TAG_BF16:
-          block_acc<TAG_BF16, NR, MB, A>(reinterpret_cast<const uint16_t *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
-                                      Q * NR, valid, acc);
-          break;
-        default:
-          block_acc<TAG_Q43, NR, MB, A>(reinterpret_cast<const uint8_t *>(wst) + e0, xst + q * NR, cnt, Q * ct, slots,
-                                     Q * NR, valid, acc);
-          break;
-      }
+      dispatch_tag(m.b, [&](auto t) {
+        constexpr int TG = decltype(t)::value;
+        block_acc<TG, NR, MB, A>(reinterpret_cast<const typename Elem<TG>::T *>(wst) + e0, xst + q * NR, cnt, Q * ct,
+                                 slots, Q * NR, valid, acc);
+      });
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -931,13 +964,9 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
       const double *zst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
       int kfirst = ks - kbase;
       if (kfirst < 0) kfirst += KS;
-      switch (m.b & 0xff) {
-        case TAG_FP64: p2_mma_cols<TAG_FP64, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
-        case TAG_FP32: p2_mma_cols<TAG_FP32, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
-        case TAG_FP16: p2_mma_cols<TAG_FP16, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
-        case TAG_BF16: p2_mma_cols<TAG_BF16, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
-        default: p2_mma_cols<TAG_Q43, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c); break;
-      }
+      dispatch_tag(m.b & 0xff, [&](auto t) {
+        p2_mma_cols<decltype(t)::value, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c);
+      });
     }
     if (KS == 1) {
       kbase = 0;
@@ -1180,28 +1209,11 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
       const int ncols = m.r1 - m.r0;
       const int cnt = g < ncols ? (ncols - g + Gn - 1) / Gn : 0;
       const int e0 = g * nr + rr;
-      switch (m.b & 0xff) {
-        case TAG_FP64:
-          block_acc<TAG_FP64, NR, MB, A>(reinterpret_cast<const double *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
-                                      Gn * NR, valid, acc);
-          break;
-        case TAG_FP32:
-          block_acc<TAG_FP32, NR, MB, A>(reinterpret_cast<const float *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
-                                      Gn * NR, valid, acc);
-          break;
-        case TAG_FP16:
-          block_acc<TAG_FP16, NR, MB, A>(reinterpret_cast<const __half *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
-                                      Gn * NR, valid, acc);
-          break;
-        case TAG_BF16:
-          block_acc<TAG_BF16, NR, MB, A>(reinterpret_cast<const uint16_t *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
-                                      Gn * NR, valid, acc);
-          break;
-        default:
-          block_acc<TAG_Q43, NR, MB, A>(reinterpret_cast<const uint8_t *>(ust) + e0, zst + g * NR, cnt, Gn * nr, nr2,
-                                     Gn * NR, valid, acc);
-          break;
-      }
+      dispatch_tag(m.b & 0xff, [&](auto t) {
+        constexpr int TG = decltype(t)::value;
+        block_acc<TG, NR, MB, A>(reinterpret_cast<const typename Elem<TG>::T *>(ust) + e0, zst + g * NR, cnt,
+                                 Gn * nr, nr2, Gn * NR, valid, acc);
+      });
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);

@@ -16,13 +16,13 @@ LIB_PATH = os.environ.get("HH_LIB") or os.path.join(_HERE, "libhh.so")   # HH_LI
 
 HH_OK, HH_EINVAL, HH_ENOMEM, HH_ECUDA, HH_ENUMERIC, HH_EDEPTH, HH_EUNSUPPORTED = range(7)
 K_LOG, K_INV_R, K_INV_R2, K_GAUSS, K_EXP = range(5)
-P_FP64, P_FP32, P_FP16, P_BF16, P_Q43 = 1, 2, 4, 8, 16
+P_FP64, P_FP32, P_FP16, P_BF16, P_Q43, P_BF24, P_FP48 = 1, 2, 4, 8, 16, 32, 64
 P_MIXED = 15
-NTAG = 5                                   # tags 0..4 = fp64, fp32, fp16, bf16, q43
+NTAG = 7                                   # tags 0..6 = fp64, fp32, fp16, bf16, q43, bf24, fp48
 LEDGER_ONLY = 1 << 16
 TIE_FP16 = 1 << 17
 SWITCH_NONE = -1
-ARENA_W, ARENA_U, ARENA_D = 0, 5, 10
+ARENA_W, ARENA_U, ARENA_D = 0, 7, 14
 
 
 class HHError(RuntimeError):
@@ -42,8 +42,8 @@ class hh_info_t(C.Structure):
         ("precision_set", C.c_uint32), ("ledger_only", C.c_int32),
         ("n_cells", C.c_int64), ("nblocks", C.c_int64), ("n_lowrank", C.c_int64), ("n_dense", C.c_int64),
         ("total_rank", C.c_int64), ("norm2", C.c_double),
-        ("w_bytes", C.c_int64 * 5), ("u_bytes", C.c_int64 * 5), ("d_bytes", C.c_int64),
-        ("stored_bytes", C.c_int64), ("stored_bytes_tag", C.c_int64 * 6), ("padded_bytes", C.c_int64),
+        ("w_bytes", C.c_int64 * 7), ("u_bytes", C.c_int64 * 7), ("d_bytes", C.c_int64),
+        ("stored_bytes", C.c_int64), ("stored_bytes_tag", C.c_int64 * 8), ("padded_bytes", C.c_int64),
         ("c_far", C.c_int32), ("c_nbr", C.c_int32), ("c_sib", C.c_int32),
         ("n_fallback", C.c_int64), ("n_promoted", C.c_int64), ("n_coincident", C.c_int64), ("n_retry", C.c_int64),
         ("build_seconds", C.c_double), ("n_inexact", C.c_int64),

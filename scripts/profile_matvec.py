@@ -47,7 +47,7 @@ ls = ex["leaf_start"]
 sh = info["d"] * (info["L"] - B["level"].astype(np.int64))
 m = ls[(B["tgt"] + 1) << sh] - ls[B["tgt"] << sh]
 n = ls[(B["src"] + 1) << sh] - ls[B["src"] << sh]
-wb = np.array([8, 4, 2, 2, 1])[B["tag"]]
+wb = np.array([8, 4, 2, 2, 1, 3, 6])[B["tag"]]
 lr = B["storage"] == 0
 p = B["rank"].astype(np.int64)
 w1 = int(np.sum((p * n * wb)[lr]))

@@ -21,7 +21,7 @@ from paper_2604_09147_b200 import hh  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SMALL = ["2d_tiny", "2d_fig8_e4", "2d_fig8_e2", "3d_small_inv_r", "3d_small_exp", "3d_sphere_small", "2d_circle_small",
-         "1d_log", "2d_fig8_e2_q43", "3d_small_exp_q43"]
+         "1d_log", "2d_fig8_e2_q43", "3d_small_exp_q43", "3d_small_inv_r_acc", "2d_tiny_acc"]
 
 
 @pytest.fixture(scope="module", params=SMALL)
@@ -132,7 +132,7 @@ def test_determinism_bitwise(built):
 def test_rounding_routines_match_oracle():
     rng = np.random.default_rng(5)
     base = rng.standard_normal(5000) * np.exp2(rng.integers(-140, 130, 5000))
-    for tag in (F.FP32, F.FP16, F.BF16, F.Q43):
+    for tag in (F.FP32, F.FP16, F.BF16, F.Q43, F.BF24):
         r = F.round_rne(base, tag)
         fin = np.isfinite(r) & (r != 0)
         m, emin, _ = F.PARAMS[tag]
@@ -143,6 +143,8 @@ def test_rounding_routines_match_oracle():
         xs = xs[np.isfinite(xs)]
         got = hh.selftest_round(xs, tag)
         ref = F.to_storage_bits(xs, tag).astype(np.uint32)
+        if tag == F.BF24:     # three little-endian bytes -> the 24-bit pattern
+            ref = ref[:, 0] | (ref[:, 1] << np.uint32(8)) | (ref[:, 2] << np.uint32(16))
         np.testing.assert_array_equal(got, ref)
 
 

@@ -53,7 +53,7 @@ def test_packing_function_matches_oracle(d, L, eta):
         storage = dense.astype(np.uint8)
         rank = np.where(dense, 0, rng.integers(0, 40, nb)).astype(np.int32)
         rank[rng.random(nb) < 0.05] = 0                      # some rank-0 low-rank blocks
-        tag = np.where(dense, 0, rng.integers(0, 5, nb)).astype(np.uint8)
+        tag = np.where(dense, 0, rng.integers(0, 7, nb)).astype(np.uint8)
         ref = PK.pack(tr.leaf_start, d, L, part.level, part.tgt, part.src, rank, tag, storage)
         got = hh.selftest_layout(tr.leaf_start, d, L, part.level, part.tgt, part.src, rank, tag, storage)
         lr = storage == 0
@@ -77,7 +77,8 @@ def test_tagging_matches_oracle(d, L, eta):
     from oracle import hmatrix as HM
     rng = np.random.default_rng(11 * d + L)
     tr = _tree(d, L, rng, p_empty=0.2, mean=7)
-    edges = [240.0, 247.99, 248.0, 65504.0, 65519.99, 65520.0, float.fromhex("0x1.fep127"), float.fromhex("0x1.ffp127"),
+    edges = [240.0, 247.99, 248.0, 65504.0, 65519.99, 65520.0, float.fromhex("0x1.fffe8p127"),
+             float.fromhex("0x1.ffffp127"), float.fromhex("0x1.fep127"), float.fromhex("0x1.ffp127"),
              float.fromhex("0x1.fffffep127"), float.fromhex("0x1.ffffffp127"), 1e39, 1e300]
     for s in (PT.SWITCH_NONE, max(0, L - 1)):
         part = PT.build_partition(tr, eta, s)
@@ -91,7 +92,8 @@ def test_tagging_matches_oracle(d, L, eta):
         maxabs = np.exp(rng.uniform(-5, 12, nb))
         hit = rng.random(nb) < 0.15
         maxabs[hit] = rng.choice(edges, int(hit.sum()))
-        for pset in (W_MIXED, W_MIXED | (1 << 17), 1 | 4, 1 | 8, 1 | 2 | 8, 1 | 4 | 8 | (1 << 17), 1, W_MIXED | 16, 1 | 16, 1 | 4 | 16):
+        for pset in (W_MIXED, W_MIXED | (1 << 17), 1 | 4, 1 | 8, 1 | 2 | 8, 1 | 4 | 8 | (1 << 17), 1, W_MIXED | 16, 1 | 16, 1 | 4 | 16, 127, 1 | 32 | 64,
+                     W_MIXED | 32, 1 | 2 | 64):
             # hh_build compresses every block except leaf diagonals (and leaf neighbours when uniform)
             dense0 = (part.kind == PT.DIAG) | ((part.kind == PT.LNBR) & ((pset & 15) == 1))
             rk = np.where(dense0, 0, rank)

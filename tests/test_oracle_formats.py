@@ -167,3 +167,64 @@ def test_q43_storage_bits_roundtrip_and_e4m3_decode():
     np.testing.assert_array_equal(ours, ocp)
     vals, _ = _q43_values()
     np.testing.assert_array_equal(np.sort(np.unique(np.abs(ours))), np.array([float(v) for v in vals]))
+
+
+# ------------------------------------------------------------- accessor formats (NEXT-3)
+def _rne_fraction(x, m, emin):
+    """Nearest value (1 + k / 2^m) 2^e (normal) or (k / 2^m) 2^emin (subnormal) to the exact rational
+    x, ties to the even k — the definition, in exact arithmetic (no overflow in the test range)."""
+    fx = Fraction(float(x))
+    s = -1 if fx < 0 else 1
+    a = abs(fx)
+    if a == 0:
+        return 0.0
+    e = max(emin, a.numerator.bit_length() - a.denominator.bit_length())
+    while Fraction(2) ** e > a and e > emin:
+        e -= 1
+    while Fraction(2) ** (e + 1) <= a:
+        e += 1
+    q = Fraction(2) ** (e - m)                    # spacing at a
+    k = a / q
+    lo = k.numerator // k.denominator
+    rem = k - lo
+    kk = lo + 1 if (rem > Fraction(1, 2) or (rem == Fraction(1, 2) and lo % 2 == 1)) else lo
+    return float(s * kk * q)
+
+
+@pytest.mark.parametrize("tag", [F.BF24, F.FP48])
+def test_accessor_formats_rne_by_definition(tag):
+    m, emin, _ = F.PARAMS[tag]
+    rng = np.random.default_rng(tag)
+    x = rng.standard_normal(400) * np.exp2(rng.integers(-40, 40, 400))
+    r = F.round_rne(x, tag)
+    q = np.ldexp(1.0, np.maximum(np.frexp(np.abs(r))[1] - 1, emin) - m)
+    mids = r + np.sign(r) * q / 2                        # exact midpoints
+    xs = np.concatenate([x, mids, np.nextafter(mids, 0), np.nextafter(mids, np.inf)])
+    if tag == F.BF24:                                     # fp32's subnormal range, 15-bit mantissa
+        xs = np.concatenate([xs, rng.uniform(0, 2.0 ** -126, 200), [2.0 ** -141, 3 * 2.0 ** -142]])
+    got = F.round_rne(xs, tag)
+    for a, g in zip(xs, got):
+        assert g == _rne_fraction(a, m, emin), (tag, a, g)
+
+
+def test_accessor_formats_worked_examples_and_decode():
+    # bf24(0.1): 0.1 = 1.6 2^-4, 0.6 * 2^15 = 19660.8 -> 19661: (2^15 + 19661) / 2^19
+    assert F.round_rne(np.array([0.1]), F.BF24)[0] == 52429 / 2 ** 19 == 0.1000003814697265625
+    # fp48(1/3): 1/3 = (4/3) 2^-2, (1/3) 2^36 = 22906492245.33 -> 22906492245
+    assert F.round_rne(np.array([1 / 3]), F.FP48)[0] == (2 ** 36 + 22906492245) / 2 ** 38
+    # overflow: bf24 x_max = (2 - 2^-15) 2^127 = 0x1.fffep127; the midpoint (2 - 2^-16) 2^127 to
+    # 2^128 rounds to even = inf
+    assert F.x_max(F.BF24) == float.fromhex("0x1.fffep127")
+    assert F.round_rne(np.array([float.fromhex("0x1.fffe8p127")]), F.BF24)[0] == F.x_max(F.BF24)
+    assert np.isinf(F.round_rne(np.array([float.fromhex("0x1.ffffp127")]), F.BF24)[0])
+    assert F.unit_roundoff(F.BF24) == 2.0 ** -16 and F.unit_roundoff(F.FP48) == 2.0 ** -37
+    # the stored bytes are the top bytes of the IEEE pattern: decode = zero-extend and reinterpret
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(500)
+    for tag, pad, dt in ((F.BF24, 1, "<f4"), (F.FP48, 2, "<f8")):
+        b = F.to_storage_bits(x, tag).reshape(x.size, -1)
+        ref = np.array([np.frombuffer(bytes(pad) + bytes(row), dt)[0] for row in b], dtype=np.float64)
+        np.testing.assert_array_equal(F.from_storage_bytes(b.tobytes(), tag), ref)
+        np.testing.assert_array_equal(ref, F.round_rne(x, tag))
+    # Eq. 4.4's candidate order gains the two formats between the Table 1 ones
+    assert F.BY_U == (F.Q43, F.BF16, F.FP16, F.BF24, F.FP32, F.FP48, F.FP64)

@@ -140,3 +140,10 @@ FIG9_CONFIGS = {
                           eps=1e-6, pset=P_MIXED, nrhs=1, xdist="uniform_01", lo=-1.0, hi=1.0),
 }
 FIG9_EPS = [1e-2, 1e-4, 1e-6, 1e-8, 1e-10]
+
+# NEXT-3: the accessor continuum at byte granularity: bf24 (3 B, u = 2^-16) and
+# fp48 (6 B, u = 2^-37) between the Table 1 formats (precision_set bits 32 and 64)
+P_BF24, P_FP48 = 32, 64
+P_ACCESSOR = P_MIXED | P_Q43 | P_BF24 | P_FP48
+SMALL_CONFIGS["3d_small_inv_r_acc"] = dict(SMALL_CONFIGS["3d_small_inv_r"], k=23, pset=P_ACCESSOR)
+SMALL_CONFIGS["2d_tiny_acc"] = dict(CONFIGS["2d_tiny"], k=24, eps=1e-10, pset=P_ACCESSOR)
