@@ -81,6 +81,9 @@ constexpr int META = 64;
 #ifndef HH_MV_PDL
 #define HH_MV_PDL 1  // programmatic dependent launch between the matvec kernels
 #endif
+#ifndef HH_MV_P2RED
+#define HH_MV_P2RED 0  // NR = 1 leaf-end reduction: 0 = one thread per row slot, 1 = lanes per row + shuffles
+#endif
 #ifndef HH_MV_VEC1
 #define HH_MV_VEC1 1  // NR = 1 consumers with vector factor loads (0: the round-1 scalar consumers)
 #endif
@@ -1033,6 +1036,9 @@ __device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, 
                                                 int tid, int lane) {
   static_assert(sizeof(double) * NCT * 4 <= (size_t)G::WBUF, "leaf reduction fits the stage");
   int cur_nr = -1, V = 1, nslots = 1, Gn = 1, rs = 0, g = 0;
+  int lt = 0, rr = 0, sub = 0, rsl = 0, ri = 0;  // leaf-end reduction role of this thread
+  int64_t cur_leaf = -1, yi = 0;                 // the leaf's first tree position, y index of row rr
+  int64_t ys[4] = {0, 0, 0, 0};                  // (HH_MV_P2RED = 0) y indices of this slot's rows
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int n = 0;; ++n) {
     const int s = n % G::STAGES;
@@ -1048,6 +1054,24 @@ __device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, 
       Gn = NCT / nslots;  // nr <= 256 (leaf_size limit)
       rs = tid % nslots;
       g = tid / nslots;
+      // reduction: row rr of the leaf (slot rr / V, element rr % V) is summed by T = 2^lt
+      // adjacent lanes (T * nr <= NCT), each over a strided subset of the Gn group partials
+      lt = 0;
+      while (lt < 5 && (nr << (lt + 1)) <= NCT) ++lt;
+      rr = tid >> lt;
+      sub = tid & ((1 << lt) - 1);
+      rsl = rr / V;
+      ri = rr - rsl * V;
+    }
+    if (m.p != cur_leaf) {  // a new leaf: its scatter indices are fetched now, used at the leaf end
+      cur_leaf = m.p;
+#if HH_MV_P2RED
+      if (rr < nr) yi = a.perm[m.p + rr];
+#else
+      if (tid < nslots)
+        for (int i = 0; i < 4; ++i)
+          if (i < V) ys[i] = a.perm[m.p + tid * V + i];
+#endif
     }
     if (g < Gn) {
       const uint8_t *ust = st + m.wlead;
@@ -1073,23 +1097,32 @@ __device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, 
       acc[i] = 0.0;
     }
     consumer_sync();
-    {
-      // row r of the leaf = slot r / V, element r % V; T = 2^k adjacent lanes per row (T * nr <=
-      // NCT) each sum a strided subset of the Gn partials, then a fixed shuffle tree
-      int lt = 0;
-      while (lt < 5 && (nr << (lt + 1)) <= NCT) ++lt;
-      const int T = 1 << lt, r = tid >> lt, sub = tid & (T - 1);
-      double sum = 0.0;
-      if (r < nr) {
-        const int rsl = r / V, ri = r - rsl * V;
-        for (int gg = sub; gg < Gn; gg += T) sum += red[(gg * nslots + rsl) * 4 + ri];
-      }
-      for (int o = 1; o < T; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (r < nr && sub == 0) a.y[a.perm[m.p + r]] = sum;
-    }
+#if HH_MV_P2RED
+    const int T = 1 << lt;
+    double sum = 0.0;
+    if (rr < nr)
+      for (int gg = sub; gg < Gn; gg += T) sum += red[(gg * nslots + rsl) * 4 + ri];
+#else
+    double sv[4] = {0.0, 0.0, 0.0, 0.0};
+    if (tid < nslots)
+      for (int gg = 0; gg < Gn; ++gg)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < V) sv[i] += red[(gg * nslots + tid) * 4 + i];
+#endif
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     consumer_sync();
     if (lane == 0) mbar_arrive(&empty[s]);  // the stage goes back to the producer's TMA
+#if HH_MV_P2RED
+    // fixed shuffle tree over the T lanes of the row, then the scatter y[perm[t]] (a10)
+    for (int o = 1; o < T; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (rr < nr && sub == 0) a.y[yi] = sum;
+#else
+    if (tid < nslots)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < V) a.y[ys[i]] = sv[i];
+#endif
   }
 }
 
