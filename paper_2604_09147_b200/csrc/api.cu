@@ -252,9 +252,9 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
       std::vector<int32_t> zmap;
       std::vector<P1Combine> comb;
       std::vector<P2Seg> segs;
-      std::vector<P2Leaf> leaves;
+      std::vector<P2Leaf> leaves, leaves_mo;
       int64_t npartial = 0;
-      build_plan(H, tiles, zmap, comb, npartial, segs, leaves);
+      build_plan(H, tiles, zmap, comb, npartial, segs, leaves, leaves_mo);
       h2d(H->p1_tiles, tiles, st);
       h2d(H->zmap, zmap, st);
       h2d(H->p1_comb, comb, st);
@@ -263,6 +263,7 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
       H->partial.alloc(sizeof(double) * 16 * (size_t)std::max<int64_t>(1, npartial));
       h2d(H->p2_segs, segs, st);
       h2d(H->p2_leaves, leaves, st);
+      h2d(H->p2_leaves_mo, leaves_mo, st);
       H->n_p1_tiles = (int64_t)tiles.size();
       H->n_p2_leaves = (int64_t)leaves.size();
       H->v.alloc(sizeof(double) * 16 * (size_t)(N + H->ztotal) + 64);

@@ -53,7 +53,8 @@ void assign_tags(hh_matrix *H);
 void compute_layout(hh_matrix *H);
 void cluster_range(const hh_matrix *H, int l, int64_t m, int64_t &a, int64_t &n);
 void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &zmap, std::vector<P1Combine> &comb,
-                int64_t &npartial, std::vector<P2Seg> &segs, std::vector<P2Leaf> &leaves);
+                int64_t &npartial, std::vector<P2Seg> &segs, std::vector<P2Leaf> &leaves,
+                std::vector<P2Leaf> &leaves_morton);
 void run_matvec(hh_matrix *H, const double *x, double *y, int nrhs, cudaStream_t st, int wp = 0);
 void print_build_profile();
 

@@ -106,7 +106,7 @@ struct hh_matrix {
   hh::DBuf W[hh::NTAG], U[hh::NTAG], D;
   int64_t w_bytes[hh::NTAG] = {}, u_bytes[hh::NTAG] = {}, d_bytes = 0;
   // matvec plan
-  hh::DBuf p1_tiles, zmap, p2_segs, p2_leaves, p1_comb, partial;
+  hh::DBuf p1_tiles, zmap, p2_segs, p2_leaves, p2_leaves_mo, p1_comb, partial;  // leaves: LPT / Morton order
   int64_t n_p1_tiles = 0, n_p2_leaves = 0, n_p1_comb = 0, n_partial = 0;
   hh::DBuf v;        // [(N + ztotal) * 16] doubles (+ slack for 16-B aligned superset copies)
   hh::DBuf ctr;      // work counters of the persistent matvec kernels (zeroed by the gather)

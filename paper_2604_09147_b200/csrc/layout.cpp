@@ -268,7 +268,8 @@ void compute_layout(hh_matrix *H) {
 // Phase 2: per leaf, dense segments then per tag the levels' U column groups; leaves with
 // the most bytes first.
 void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &zmap, std::vector<P1Combine> &comb,
-                int64_t &npartial, std::vector<P2Seg> &segs, std::vector<P2Leaf> &leaves) {
+                int64_t &npartial, std::vector<P2Seg> &segs, std::vector<P2Leaf> &leaves,
+                std::vector<P2Leaf> &leaves_morton) {
   const size_t nb = H->level.size();
   const int d = H->d, L = H->L;
   const int64_t N = H->N;
@@ -379,9 +380,12 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
     leaves.push_back(lf);
     lbytes.push_back(bytes);
   }
-  // leaves with the most bytes first (LPT): measured ~4% faster in phase 2 than Morton order
-  // (profiles/r01_variants.txt), although Morton order re-reads fewer z slices from DRAM
-  // (ncu: LPT costs ~4% extra phase-2 DRAM reads at 3D N=2^20) — the tail balance wins
+  // Morton order (the construction order) is kept for the multi-RHS products: there z is NR
+  // times larger (5.8 GB at 3D N=2^20 and 16 RHS) and leaves processed at the same time must
+  // share their ancestors' z slices in L2 (ncu r02: in LPT order phase 2 at 16 RHS read 1.8x
+  // its U bytes from DRAM on the proxy).  At one RHS z (45 MB) stays in L2 in any order and
+  // leaves with the most bytes first (LPT) were measured ~4% faster (profiles/r01_variants.txt).
+  leaves_morton = leaves;
 #ifndef HH_P2_MORTON
   {
     std::vector<size_t> ord(leaves.size());

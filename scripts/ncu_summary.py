@@ -23,6 +23,10 @@ KEYS = [
     ("lts__t_sector_hit_rate.pct", "l2_hit_%"),
     ("smsp__inst_executed.sum", "warp_instrs"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pipe_%"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor_pipe_%"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_active_%"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem_wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem_conflicts"),
 ]
 
 
@@ -31,8 +35,8 @@ def main():
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
-    stall_cols = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warp_latency_issue_stalled_")
-                  or h.startswith("smsp__pcsamp_warps_issue_stalled_")]
+    stall_cols = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_issue_stalled_")
+                  and h.endswith("_per_issue_active.ratio")]
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")]
         print(f"== {name}")
