@@ -12,6 +12,8 @@ paper (arxiv 2604.09147, /root/reference/PAPER.md) step by step:
   hmatrix.py    Alg. 1 (H_h) + Alg. 4 (norms) + Alg. 2 (AMP)
   pack.py       arena packing function            (our layout; no paper passage)
   matvec.py     Alg. 3 (H-hat x)
+  matvec_wp.py  Alg. 3 in fp32 / fp16 working precision (G27)
+  switch_level.py  Alg. 5 (switching level l*)
   dense.py      dense A x and ||A||_F (definition)
   metrics.py    error metrics and the Thm 4.2 / 4.4 bounds
 
@@ -49,6 +51,9 @@ value or a brute force — never a retyping of the function):
   pack.pack                              no byte written twice, round trip, z contiguity  test_oracle_hmatrix
                                          (our layout: no paper passage; the C++ twin is compared in test_host_logic)
   matvec.matvec                          dense reconstruction, L=0 dense gemv, Thm 4.4  test_oracle_hmatrix
+  matvec_wp.matvec_wp (NEXT-3, G27)      hand-worked fp16/fp32 sums (2049 ones -> 2048), operands
+                                         rounded once, exact on integer data, within the a priori
+                                         rounding bound of the exact product           test_oracle_matvec_wp
   dense / metrics                        definitions; bound constants at eta=sqrt(d) = 27/8/3, 189/26/7
 
 Parity unpinned: exact per-block ranks and tags at 3D scale (the paper prints none) — checked

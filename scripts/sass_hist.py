@@ -47,9 +47,12 @@ def main():
     print(f"# SASS instruction histogram of {LIB} (cuobjdump -sass); columns: " + " ".join(["total"] + KEYS))
     for f, c in funcs.items():
         nm = names.get(f, f)
-        nm = re.sub(r"\(.*", "", nm)
+        nm = nm.replace("(anonymous namespace)::", "")
+        nm = re.sub(r"^void ", "", nm)
+        nm = re.sub(r"\((?:[^()]|\([^()]*\))*\)$", "", nm)  # drop the parameter list only
+        nm = re.sub(r"CUB_\d+_SM_\d+::", "", nm)
         row = [str(c["_total"])] + [str(c[k]) for k in KEYS]
-        print(f"{nm[:60]:60s} " + " ".join(row))
+        print(f"{nm[:72]:72s} " + " ".join(row))
 
 
 if __name__ == "__main__":
