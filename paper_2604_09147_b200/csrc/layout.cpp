@@ -290,8 +290,24 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
     return H->wcol[a] < H->wcol[c];
   });
   std::vector<int64_t> tbytes;
-  // row-split threshold (HH_P1_ROWS lowers it so tests exercise the split on small inputs)
-  static const int64_t split_rows = getenv("HH_P1_ROWS") ? std::max(1ll, atoll(getenv("HH_P1_ROWS"))) : P1_ROWS;
+  // Row-split threshold.  A piece should stay below the average share of one resident CTA
+  // (~444 on a B200), or the phase ends on a few CTAs still streaming a coarse-level panel:
+  // at 2D N=65536 (0.35 GB of W, 4096-row level-2 panels) pieces of 4096 rows took 0.087 ms,
+  // pieces of 512 rows 0.071 ms (profiles/r02f_2d_rowsplit_ab.txt).  Large problems keep
+  // P1_ROWS.  HH_P1_ROWS overrides it (tests exercise the split on small inputs).
+  int64_t split_rows = P1_ROWS;
+  if (getenv("HH_P1_ROWS")) {
+    split_rows = std::max(1ll, atoll(getenv("HH_P1_ROWS")));
+  } else {
+    int64_t wtotal = 0;
+    for (const size_t b : idx) {
+      int64_t j0, n;
+      cluster_range(H, H->level[b], H->src[b], j0, n);
+      wtotal += n * H->rank[b] * tag_bytes(H->tag[b]);
+    }
+    const int64_t share_rows = wtotal / 444 / (W_CT * 4);  // rows of a full fp32 tile in one CTA's share
+    while (split_rows > 512 && split_rows > share_rows) split_rows >>= 1;
+  }
   size_t i = 0;
   while (i < idx.size()) {
     size_t e = i;
@@ -379,6 +395,32 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
     lf.s1 = (int64_t)segs.size();
     leaves.push_back(lf);
     lbytes.push_back(bytes);
+  }
+  // Stage geometry of the single-RHS kernels (matvec.cu Geo): when the plan's stage windows are
+  // mostly small (2D trees: ~16-point leaves, a few KiB per (level, tag) column group), twice
+  // the stages at half the size keep more bytes in flight.  Decided per phase from the mean
+  // window fill under the default geometry (32 KiB factor windows, 512 vector entries);
+  // HH_MV_GEOM1 / HH_MV_GEOM2 = 0 / 1 override it.
+  {
+    int64_t w1 = 0, b1 = 0, w2 = 0, b2 = 0;
+    for (size_t k = 0; k < tiles.size(); ++k) {
+      const int64_t rowb = (int64_t)tiles[k].ct * tag_bytes(tiles[k].tag);
+      const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(512, 32768 / rowb));
+      w1 += (tiles[k].n + rs - 1) / rs;
+      b1 += tiles[k].n * rowb;
+    }
+    for (const P2Leaf &lf : leaves)
+      for (int64_t si = lf.s0; si < lf.s1; ++si) {
+        const int64_t colb = (int64_t)lf.nr * tag_bytes(segs[si].tag);
+        const int64_t cs = std::max<int64_t>(1, std::min<int64_t>(512, 32768 / colb));
+        w2 += (segs[si].ncols + cs - 1) / cs;
+        b2 += segs[si].ncols * colb;
+      }
+    const int64_t small_fill = 12288;
+    H->geom[0] = w1 > 0 && b1 / w1 < small_fill;
+    H->geom[1] = w2 > 0 && b2 / w2 < small_fill;
+    if (getenv("HH_MV_GEOM1")) H->geom[0] = atoi(getenv("HH_MV_GEOM1")) != 0;
+    if (getenv("HH_MV_GEOM2")) H->geom[1] = atoi(getenv("HH_MV_GEOM2")) != 0;
   }
   // Morton order (the construction order) is kept for the multi-RHS products: there z is NR
   // times larger (5.8 GB at 3D N=2^20 and 16 RHS) and leaves processed at the same time must

@@ -91,27 +91,67 @@ constexpr int META = 64;
 #define HH_MV_VEC1 1  // NR = 1 consumers with vector factor loads (0: the round-1 scalar consumers)
 #endif
 
+// K-quartered stages for the DMMA consumers (NR = 8, 16).  A DMMA K-step takes four K
+// indices, one per lane group kq = lane % 4.  With the window staged as one linear copy the
+// four indices are consecutive, so the four kq lanes of a fragment load addresses one
+// row (x~ / z: NR * 8 B = 128 B at NR = 16) or one U column (|R| * w B, 128 B for a 32-point
+// fp32 leaf) apart — the same shared-memory banks, a 4-way conflict on every fragment load
+// (ncu r02f, proxy at 16 RHS: 180 M of 270 M phase-2 wavefronts were conflict replays, the
+// LSU pipe 69% busy next to a 75% busy DMMA pipe).  Instead the producer cuts each window's
+// K range into four quarters, copies each with its own bulk copy to a shared-memory region
+// whose start is skewed by 32 B (8 banks) per quarter, and lane group kq walks quarter kq:
+// the four lanes of a fragment row then sit 8 banks apart, the eight rows fill the gaps.
+#ifndef HH_MV_QUART
+#define HH_MV_QUART 1
+#endif
+// byte stride between the quarter regions of a stage: room for the quarter's enclosing 16-B
+// aligned window, rounded to the 128-B bank period, plus the 32-B skew
+__host__ __device__ constexpr int quarter_stride(int qbytes) { return ((qbytes + 32 + 127) & ~127) + 32; }
+// largest quarter (bytes) whose four regions fit a buffer of BUF bytes
+constexpr int quarter_max_bytes(int buf) { return ((buf / 4 - 32) / 128) * 128 - 32; }
+
 // FP64 tensor-core (DMMA m8n8k4) consumers for the multi-RHS contractions (NR = 8, 16):
 // the phase-1 tile is then D = W^T X (ct x NR) and the phase-2 leaf Y = U Z (nr x NR).
 #ifndef HH_MV_MMA
 #define HH_MV_MMA 1
 #endif
 template <int NR> constexpr bool use_mma() { return HH_MV_MMA && (NR == 8 || NR == 16); }
+// resident CTAs per SM the register allocation must allow: the DMMA kernels are sized (shared
+// memory) for two, which 9 warps reach only at <= 96 registers per thread
+// (phase 1 at NR = 8 has 74 KiB of stages: three CTAs, <= 72 registers)
+template <int NR, int PH> constexpr int min_ctas() { return use_mma<NR>() ? (NR == 8 && PH == 1 ? 3 : 2) : HH_MV_MINB; }
+template <int NR, int WP = 0> constexpr bool quartered() { return HH_MV_QUART && WP == 0 && use_mma<NR>(); }
 
-template <int NR, int PH> struct Geo {  // PH = phase (1: x~ rows per W row window, 2: z per U column)
+// GV = geometry variant, chosen per handle and phase (hh_matrix::geom): 0 = few large stages
+// (the measured winner when items fill them: 3D configs), 1 = twice the stages at half the size
+// for small-item plans (2D trees with ~16-point leaves: most windows hold < 12 KiB, so two
+// 32 KiB stages per CTA leave too few bytes in flight), NR = 1 only.
+#ifndef HH_MV_SMALL_W
+#define HH_MV_SMALL_W 16384
+#endif
+#ifndef HH_MV_SMALL_X
+#define HH_MV_SMALL_X 2048
+#endif
+#ifndef HH_MV_SMALL_STAGES
+#define HH_MV_SMALL_STAGES 4
+#endif
+template <int NR, int PH, int GV = 0> struct Geo {  // PH = phase (1: x~ rows per W row window, 2: z per U column)
+  static_assert(GV == 0 || NR == 1, "the small-item geometry is built for one RHS");
   // factor bytes per stage (phase 2 at NR >= 8 may use smaller stages to fit 2 CTAs/SM)
-  static constexpr int WDATA = (PH == 2 && NR >= 16) ? HH_MV_P2HI : (PH == 1 && NR >= 16) ? HH_MV_P1HI : HH_MV_WDATA;
+  static constexpr int WDATA = GV == 1 ? HH_MV_SMALL_W
+                               : (PH == 2 && NR >= 16) ? HH_MV_P2HI : (PH == 1 && NR >= 16) ? HH_MV_P1HI : HH_MV_WDATA;
   static constexpr int WBUF = WDATA + 32;                            // + 16-B alignment slack
   // vector bytes per stage: phase 1 needs one NR-vector per W row (a 248-column row is >= 1 KiB
   // of factors), phase 2 one per U column (|R| rows, as little as ~32 elements)
   static constexpr int XDATA =
-      NR <= 2 ? HH_MV_XDATA
+      GV == 1 ? HH_MV_SMALL_X
+      : NR <= 2 ? HH_MV_XDATA
               : (PH == 1 ? ((NR >= 16 && HH_MV_P1X > 0) ? HH_MV_P1X : (NR * 512 > 4096 ? NR * 512 : 4096))
                          : ((NR >= 16 && HH_MV_P2X > 0) ? HH_MV_P2X : NR * 2048 / (32768 / WDATA)));
   static constexpr int XELEMS = XDATA / 8;                        // doubles (rows x NR)
   static constexpr int XBUF = XDATA + 32;
   static constexpr int STAGE = WBUF + XBUF + META;
-  static constexpr int STAGES = (PH == 2 && NR >= 16) ? HH_MV_P2STAGES : HH_MV_STAGES;
+  static constexpr int STAGES = GV == 1 ? HH_MV_SMALL_STAGES : (PH == 2 && NR >= 16) ? HH_MV_P2STAGES : HH_MV_STAGES;
   // phase 2 at NR = 16 may reduce in the leaf's last stage (held until the reduction ends)
   static constexpr bool RED_IN_STAGE = PH == 2 && NR >= 16 && HH_MV_P2ALIAS && use_mma<NR>();
   static constexpr size_t red_bytes() {  // phase-2 cross-group reduction buffer
@@ -485,6 +525,63 @@ __device__ __forceinline__ void p1_mma_rows_t(const uint8_t *wst, const double *
   }
 }
 
+// K-quartered phase-1 K-loop (HH_MV_QUART): the window's rows [0, nrows) lie in four quarter
+// regions of Qr = ceil(nrows / 4) rows each (the last ones shorter or empty); lane group kq
+// multiplies row j of quarter kq in K-step j.  wq / xq point at this lane's quarter.
+template <int TAG, int NR, int MT>
+__device__ __forceinline__ void p1_mma_rows_qt(const uint8_t *wq, const double *xq, int nrq, int Qr, int ct, int col0,
+                                               int lane, double (&c)[4][NR / 8][2]) {
+  using T = typename Elem<TAG>::T;
+  const int mq = lane >> 2;
+  const T *W = reinterpret_cast<const T *>(wq) + col0 + mq;
+  const double *X = xq + mq;
+  bool cv[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) cv[mt] = col0 + mt * 8 + mq < ct;
+  int j = 0;
+  if (col0 + MT * 8 <= ct) {  // whole M-tiles: no column checks on the rows every quarter holds
+    const int jfull = __reduce_min_sync(0xffffffffu, nrq);
+#pragma unroll 2
+    for (; j < jfull; ++j) {
+      double b[NR / 8];
+#pragma unroll
+      for (int nt = 0; nt < NR / 8; ++nt) b[nt] = X[j * NR + nt * 8];
+      const T *wrow = W + j * ct;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const double av = up<TAG>(wrow[mt * 8]);
+#pragma unroll
+        for (int nt = 0; nt < NR / 8; ++nt) dmma(c[mt][nt], av, b[nt]);
+      }
+    }
+  }
+#pragma unroll 2
+  for (; j < Qr; ++j) {
+    const bool rv = j < nrq;
+    double b[NR / 8];
+#pragma unroll
+    for (int nt = 0; nt < NR / 8; ++nt) b[nt] = rv ? X[j * NR + nt * 8] : 0.0;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const double av = (rv && cv[mt]) ? up<TAG>(W[j * ct + mt * 8]) : 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NR / 8; ++nt) dmma(c[mt][nt], av, b[nt]);
+    }
+  }
+}
+
+template <int TAG, int NR>
+__device__ __forceinline__ void p1_mma_rows_q(const uint8_t *wq, const double *xq, int nrq, int Qr, int ct, int col0,
+                                              int lane, double (&c)[4][NR / 8][2]) {
+  const int mtiles = min(4, (ct - col0 + 7) >> 3);
+  switch (mtiles) {
+    case 4: p1_mma_rows_qt<TAG, NR, 4>(wq, xq, nrq, Qr, ct, col0, lane, c); break;
+    case 3: p1_mma_rows_qt<TAG, NR, 3>(wq, xq, nrq, Qr, ct, col0, lane, c); break;
+    case 2: p1_mma_rows_qt<TAG, NR, 2>(wq, xq, nrq, Qr, ct, col0, lane, c); break;
+    default: p1_mma_rows_qt<TAG, NR, 1>(wq, xq, nrq, Qr, ct, col0, lane, c); break;
+  }
+}
+
 // only the M-tiles that hold columns of the tile are multiplied (MT = 1..4, warp-uniform)
 template <int TAG, int NR>
 __device__ __forceinline__ void p1_mma_rows(const uint8_t *wst, const double *xst, int nrows, int ct, int col0,
@@ -522,10 +619,21 @@ __device__ __forceinline__ void p1_mma_consumer(const P1Args &a, uint8_t *smem, 
       }
     }
     if (active) {
-      const uint8_t *wst = st + m.wlead;
-      const double *xst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
       const int nrows = m.r1 - m.r0;
-      dispatch_tag(m.b, [&](auto t) { p1_mma_rows<decltype(t)::value, NR>(wst, xst, nrows, ct, col0, lane, c); });
+      if constexpr (quartered<NR>()) {
+        // this lane's quarter: rows [kq Qr, kq Qr + nrq) of the window, staged in region kq
+        const int kq = lane & 3, Qr = (nrows + 3) >> 2;
+        const int nrq = max(0, min(Qr, nrows - kq * Qr));
+        const int qw = Qr * ct * tag_bytes(m.b), qx = Qr * NR * 8;
+        const uint8_t *wq = st + kq * quarter_stride(qw) + ((m.wlead + kq * qw) & 15);
+        const double *xq =
+            reinterpret_cast<const double *>(st + G::WBUF + kq * quarter_stride(qx) + ((m.xlead + kq * qx) & 15));
+        dispatch_tag(m.b, [&](auto t) { p1_mma_rows_q<decltype(t)::value, NR>(wq, xq, nrq, Qr, ct, col0, lane, c); });
+      } else {
+        const uint8_t *wst = st + m.wlead;
+        const double *xst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
+        dispatch_tag(m.b, [&](auto t) { p1_mma_rows<decltype(t)::value, NR>(wst, xst, nrows, ct, col0, lane, c); });
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -712,10 +820,10 @@ __device__ __forceinline__ void p1_consumer_nr1(const P1Args &a, uint8_t *smem, 
   }
 }
 
-template <int NR, int WP = 0>
-__global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
+template <int NR, int WP = 0, int GV = 0>
+__global__ void __launch_bounds__(THREADS, min_ctas<NR, 1>()) k_phase1(P1Args a) {
   static_assert(WP == 0 || NR <= 4, "reduced working precision runs the FMA consumers (NR <= 4)");
-  using G = Geo<NR, 1>;
+  using G = Geo<NR, 1, GV>;
   using A = typename WpT<WP>::A;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
@@ -746,7 +854,12 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
       if (nxt < a.ntiles) Tn = a.tiles[nxt];
       const int w = tag_bytes(T.tag);
       const int rowb = T.ct * w;
-      const int rs = max(1, min(G::XELEMS / NR, G::WDATA / rowb));
+      int rs = max(1, min(G::XELEMS / NR, G::WDATA / rowb));
+      if constexpr (quartered<NR, WP>()) {  // four quarter regions per buffer; whole K-steps per quarter
+        int Q = max(1, min(quarter_max_bytes(G::WBUF) / rowb, quarter_max_bytes(G::XBUF) / (NR * 8)));
+        if (Q >= 4) Q &= ~3;  // quarters start 16-B aligned alike => exact 8-bank skew
+        rs = 4 * Q;
+      }
       const uint8_t *wbase = pick(a.W, T.tag) + T.src + (int64_t)T.r0 * rowb;
       const uint8_t *xbase = reinterpret_cast<const uint8_t *>(a.v + (T.x0 + T.r0) * NR);
       for (int r0 = 0; r0 < T.n; r0 += rs, ++n) {
@@ -769,10 +882,29 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase1(P1Args a) {
         m->p = T.zbase;
         m->q = T.n;
         m->pb = T.pbase;
-        mbar_expect_tx(&full[s], window_bytes(wsrc, wlen) + window_bytes(xsrc, xlen));
-        uint32_t tx = 0;
-        stage_copy(st, wsrc, wlen, &full[s], pol_w, tx);
-        stage_copy(st + G::WBUF, xsrc, xlen, &full[s], pol_x, tx);
+        if constexpr (quartered<NR, WP>()) {
+          const int nrw = r1 - r0, Qr = (nrw + 3) >> 2;
+          const int qw = Qr * rowb, qx = Qr * NR * 8;
+          uint32_t exp = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int nq = max(0, min(Qr, nrw - q * Qr));
+            exp += window_bytes(wsrc + q * qw, (int64_t)nq * rowb) + window_bytes(xsrc + q * qx, (int64_t)nq * NR * 8);
+          }
+          mbar_expect_tx(&full[s], exp);
+          uint32_t tx = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int nq = max(0, min(Qr, nrw - q * Qr));
+            stage_copy(st + q * quarter_stride(qw), wsrc + q * qw, (int64_t)nq * rowb, &full[s], pol_w, tx);
+            stage_copy(st + G::WBUF + q * quarter_stride(qx), xsrc + q * qx, (int64_t)nq * NR * 8, &full[s], pol_x, tx);
+          }
+        } else {
+          mbar_expect_tx(&full[s], window_bytes(wsrc, wlen) + window_bytes(xsrc, xlen));
+          uint32_t tx = 0;
+          stage_copy(st, wsrc, wlen, &full[s], pol_w, tx);
+          stage_copy(st + G::WBUF, xsrc, xlen, &full[s], pol_x, tx);
+        }
       }
       item = nxt;
     }
@@ -923,6 +1055,45 @@ __device__ __forceinline__ void p2_mma_cols_t(const uint8_t *ust, const double *
   }
 }
 
+// K-quartered phase-2 K-loop (HH_MV_QUART): the window's columns [0, ncols) lie in four
+// quarter regions of Qc = ceil(ncols / 4) columns; lane group kq multiplies column j of
+// quarter kq in K-step j (K-steps j = kfirst, kfirst + KS, ... belong to this warp's K-slice).
+template <int TAG, int NR, int MT>
+__device__ __forceinline__ void p2_mma_cols_qt(const uint8_t *uq, const double *zq, int ncq, int Qc, int nr, int row0,
+                                               int kfirst, int KS, int lane, double (&c)[4][NR / 8][2]) {
+  using T = typename Elem<TAG>::T;
+  const int mq = lane >> 2;
+  const T *U = reinterpret_cast<const T *>(uq) + row0 + mq;
+  const double *Z = zq + mq;
+  bool rv[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) rv[mt] = row0 + mt * 8 + mq < nr;
+#pragma unroll 2
+  for (int j = kfirst; j < Qc; j += KS) {
+    const bool cvl = j < ncq;
+    double b[NR / 8];
+#pragma unroll
+    for (int nt = 0; nt < NR / 8; ++nt) b[nt] = cvl ? Z[j * NR + nt * 8] : 0.0;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const double av = (cvl && rv[mt]) ? up<TAG>(U[j * nr + mt * 8]) : 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NR / 8; ++nt) dmma(c[mt][nt], av, b[nt]);
+    }
+  }
+}
+
+template <int TAG, int NR>
+__device__ __forceinline__ void p2_mma_cols_q(const uint8_t *uq, const double *zq, int ncq, int Qc, int nr, int row0,
+                                              int tcount, int kfirst, int KS, int lane, double (&c)[4][NR / 8][2]) {
+  switch (tcount) {
+    case 4: p2_mma_cols_qt<TAG, NR, 4>(uq, zq, ncq, Qc, nr, row0, kfirst, KS, lane, c); break;
+    case 3: p2_mma_cols_qt<TAG, NR, 3>(uq, zq, ncq, Qc, nr, row0, kfirst, KS, lane, c); break;
+    case 2: p2_mma_cols_qt<TAG, NR, 2>(uq, zq, ncq, Qc, nr, row0, kfirst, KS, lane, c); break;
+    default: p2_mma_cols_qt<TAG, NR, 1>(uq, zq, ncq, Qc, nr, row0, kfirst, KS, lane, c); break;
+  }
+}
+
 // only this group's M-tiles are multiplied (tcount = 1..4, warp-uniform)
 template <int TAG, int NR>
 __device__ __forceinline__ void p2_mma_cols(const uint8_t *ust, const double *zst, int ncols, int nr, int row0,
@@ -966,13 +1137,26 @@ __device__ __forceinline__ void p2_mma_consumer(const P2Args &a, uint8_t *smem, 
     const bool active = warp < MG * KS;
     const int ncols = m.r1 - m.r0;
     if (active) {
-      const uint8_t *ust = st + m.wlead;
-      const double *zst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
       int kfirst = ks - kbase;
       if (kfirst < 0) kfirst += KS;
-      dispatch_tag(m.b & 0xff, [&](auto t) {
-        p2_mma_cols<decltype(t)::value, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c);
-      });
+      if constexpr (quartered<NR>()) {
+        // this lane's quarter: columns [kq Qc, kq Qc + ncq) of the window, staged in region kq
+        const int kq = lane & 3, Qc = (ncols + 3) >> 2;
+        const int ncq = max(0, min(Qc, ncols - kq * Qc));
+        const int qu = Qc * nr * tag_bytes(m.b & 0xff), qz = Qc * NR * 8;
+        const uint8_t *uq = st + kq * quarter_stride(qu) + ((m.wlead + kq * qu) & 15);
+        const double *zq =
+            reinterpret_cast<const double *>(st + G::WBUF + kq * quarter_stride(qz) + ((m.xlead + kq * qz) & 15));
+        dispatch_tag(m.b & 0xff, [&](auto t) {
+          p2_mma_cols_q<decltype(t)::value, NR>(uq, zq, ncq, Qc, nr, tbeg * 8, tcnt, kfirst, KS, lane, c);
+        });
+      } else {
+        const uint8_t *ust = st + m.wlead;
+        const double *zst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
+        dispatch_tag(m.b & 0xff, [&](auto t) {
+          p2_mma_cols<decltype(t)::value, NR>(ust, zst, ncols, nr, tbeg * 8, tcnt, kfirst, KS, lane, c);
+        });
+      }
     }
     if (KS == 1) {
       kbase = 0;
@@ -1129,10 +1313,10 @@ __device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, 
   }
 }
 
-template <int NR, int WP = 0>
-__global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
+template <int NR, int WP = 0, int GV = 0>
+__global__ void __launch_bounds__(THREADS, min_ctas<NR, 2>()) k_phase2(P2Args a) {
   static_assert(WP == 0 || NR <= 4, "reduced working precision runs the FMA consumers (NR <= 4)");
-  using G = Geo<NR, 2>;
+  using G = Geo<NR, 2, GV>;
   using A = typename WpT<WP>::A;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
@@ -1167,7 +1351,12 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
         if (si + 1 < Lf.s1) Sn = a.segs[si + 1];
         const int w = tag_bytes(S.tag);
         const int colb = Lf.nr * w;
-        const int cs = max(1, min(G::XELEMS / NR, G::WDATA / colb));
+        int cs = max(1, min(G::XELEMS / NR, G::WDATA / colb));
+        if constexpr (quartered<NR, WP>()) {  // four quarter regions per buffer; whole K-steps per quarter
+          int Q = max(1, min(quarter_max_bytes(G::WBUF) / colb, quarter_max_bytes(G::XBUF) / (NR * 8)));
+          if (Q >= 4) Q &= ~3;  // quarters start 16-B aligned alike => exact 8-bank skew
+          cs = 4 * Q;
+        }
         const uint8_t *ubase = (S.dense ? a.D : pick(a.U, S.tag)) + S.src;
         const uint8_t *zbase = reinterpret_cast<const uint8_t *>(a.v + S.vbeg * NR);
         for (int c0 = 0; c0 < S.ncols; c0 += cs, ++n) {
@@ -1189,10 +1378,29 @@ __global__ void __launch_bounds__(THREADS, HH_MV_MINB) k_phase2(P2Args a) {
           m->a = Lf.nr;
           m->b = S.tag | (S.dense << 8);
           m->p = Lf.r0;
-          mbar_expect_tx(&full[s], window_bytes(usrc, ulen) + window_bytes(zsrc, zlen));
-          uint32_t tx = 0;
-          stage_copy(st, usrc, ulen, &full[s], pol_w, tx);
-          stage_copy(st + G::WBUF, zsrc, zlen, &full[s], pol_x, tx);
+          if constexpr (quartered<NR, WP>()) {
+            const int nc = c1 - c0, Qc = (nc + 3) >> 2;
+            const int qu = Qc * colb, qz = Qc * NR * 8;
+            uint32_t exp = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int nq = max(0, min(Qc, nc - q * Qc));
+              exp += window_bytes(usrc + q * qu, (int64_t)nq * colb) + window_bytes(zsrc + q * qz, (int64_t)nq * NR * 8);
+            }
+            mbar_expect_tx(&full[s], exp);
+            uint32_t tx = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int nq = max(0, min(Qc, nc - q * Qc));
+              stage_copy(st + q * quarter_stride(qu), usrc + q * qu, (int64_t)nq * colb, &full[s], pol_w, tx);
+              stage_copy(st + G::WBUF + q * quarter_stride(qz), zsrc + q * qz, (int64_t)nq * NR * 8, &full[s], pol_x, tx);
+            }
+          } else {
+            mbar_expect_tx(&full[s], window_bytes(usrc, ulen) + window_bytes(zsrc, zlen));
+            uint32_t tx = 0;
+            stage_copy(st, usrc, ulen, &full[s], pol_w, tx);
+            stage_copy(st + G::WBUF, zsrc, zlen, &full[s], pol_x, tx);
+          }
         }
       }
       li = nxt;
@@ -1303,11 +1511,11 @@ void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t sm
   HH_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 
-template <int NR, int WP = 0>
-void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
+template <int NR, int WP, int GV1, int GV2>
+void matvec_chunk_g(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
   using namespace mv;
-  using G1 = Geo<NR, 1>;
-  using G2 = Geo<NR, 2>;
+  using G1 = Geo<NR, 1, GV1>;
+  using G2 = Geo<NR, 2, GV2>;
   // launch geometry (device attributes, smem opt-in, occupancy) once per handle, width and
   // working precision
   hh_matrix::LaunchCfg &L = H->lcfg[WP][NR == 1 ? 0 : NR == 2 ? 1 : NR == 4 ? 2 : NR == 8 ? 3 : 4];
@@ -1315,11 +1523,11 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     int dev = 0;
     HH_CUDA(cudaGetDevice(&dev));
     HH_CUDA(cudaDeviceGetAttribute(&L.nsm, cudaDevAttrMultiProcessorCount, dev));
-    HH_CUDA(cudaFuncSetAttribute(k_phase1<NR, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem(false)));
-    HH_CUDA(cudaFuncSetAttribute(k_phase2<NR, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::smem(true)));
+    HH_CUDA(cudaFuncSetAttribute(k_phase1<NR, WP, GV1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem(false)));
+    HH_CUDA(cudaFuncSetAttribute(k_phase2<NR, WP, GV2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::smem(true)));
     int p1 = 0, p2 = 0;
-    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_phase1<NR, WP>, THREADS, G1::smem(false)));
-    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_phase2<NR, WP>, THREADS, G2::smem(true)));
+    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_phase1<NR, WP, GV1>, THREADS, G1::smem(false)));
+    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_phase2<NR, WP, GV2>, THREADS, G2::smem(true)));
     L.grid1 = (int)std::min<int64_t>(H->n_p1_tiles, (int64_t)L.nsm * std::max(1, p1));
     L.grid2 = (int)std::min<int64_t>(H->n_p2_leaves, (int64_t)L.nsm * std::max(1, p2));
     L.ready = true;
@@ -1351,7 +1559,7 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     a.v = v;
     a.N = H->N;
     a.ctr = ctr;
-    launch_pdl(k_phase1<NR, WP>, (unsigned)L.grid1, THREADS, G1::smem(false), st, a);
+    launch_pdl(k_phase1<NR, WP, GV1>, (unsigned)L.grid1, THREADS, G1::smem(false), st, a);
     HH_LAUNCHED();
     if (H->n_p1_comb > 0) {
       launch_pdl(k_p1_combine<NR, WP>, (unsigned)std::min<int64_t>(H->n_p1_comb, (int64_t)nsm * 8), 256, 0, st,
@@ -1373,10 +1581,22 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   b.ldy = H->N;
   b.ctr = ctr;
   if (L.grid2 > 0) {
-    launch_pdl(k_phase2<NR, WP>, (unsigned)L.grid2, THREADS, G2::smem(true), st, b);
+    launch_pdl(k_phase2<NR, WP, GV2>, (unsigned)L.grid2, THREADS, G2::smem(true), st, b);
     HH_LAUNCHED();
   }
   mark(3);
+}
+
+// stage geometry per handle and phase (see Geo): the single-RHS fp64 product only
+template <int NR, int WP = 0>
+void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
+  if constexpr (NR == 1 && WP == 0) {
+    const int g1 = H->geom[0], g2 = H->geom[1];
+    if (g1 && g2) return matvec_chunk_g<1, 0, 1, 1>(H, x, y, col0, st);
+    if (g1) return matvec_chunk_g<1, 0, 1, 0>(H, x, y, col0, st);
+    if (g2) return matvec_chunk_g<1, 0, 0, 1>(H, x, y, col0, st);
+  }
+  matvec_chunk_g<NR, WP, 0, 0>(H, x, y, col0, st);
 }
 
 template <int WP>
