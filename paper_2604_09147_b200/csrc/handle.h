@@ -108,7 +108,6 @@ struct hh_matrix {
   // matvec plan
   hh::DBuf p1_tiles, zmap, p2_segs, p2_leaves, p2_leaves_mo, p1_comb, partial;  // leaves: LPT / Morton order
   int64_t n_p1_tiles = 0, n_p2_leaves = 0, n_p1_comb = 0, n_partial = 0;
-  int geom[2] = {0, 0};  // stage geometry of phase 1 / phase 2 at one RHS (matvec.cu Geo): 1 = small-item plan
   hh::DBuf v;        // [(N + ztotal) * 16] doubles (+ slack for 16-B aligned superset copies)
   hh::DBuf ctr;      // work counters of the persistent matvec kernels (zeroed by the gather)
   struct LaunchCfg {  // per RHS-chunk width (1, 2, 4, 8, 16): set once, reused by every hh_matvec

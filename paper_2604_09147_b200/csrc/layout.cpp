@@ -396,32 +396,6 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
     leaves.push_back(lf);
     lbytes.push_back(bytes);
   }
-  // Stage geometry of the single-RHS kernels (matvec.cu Geo): when the plan's stage windows are
-  // mostly small (2D trees: ~16-point leaves, a few KiB per (level, tag) column group), twice
-  // the stages at half the size keep more bytes in flight.  Decided per phase from the mean
-  // window fill under the default geometry (32 KiB factor windows, 512 vector entries);
-  // HH_MV_GEOM1 / HH_MV_GEOM2 = 0 / 1 override it.
-  {
-    int64_t w1 = 0, b1 = 0, w2 = 0, b2 = 0;
-    for (size_t k = 0; k < tiles.size(); ++k) {
-      const int64_t rowb = (int64_t)tiles[k].ct * tag_bytes(tiles[k].tag);
-      const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(512, 32768 / rowb));
-      w1 += (tiles[k].n + rs - 1) / rs;
-      b1 += tiles[k].n * rowb;
-    }
-    for (const P2Leaf &lf : leaves)
-      for (int64_t si = lf.s0; si < lf.s1; ++si) {
-        const int64_t colb = (int64_t)lf.nr * tag_bytes(segs[si].tag);
-        const int64_t cs = std::max<int64_t>(1, std::min<int64_t>(512, 32768 / colb));
-        w2 += (segs[si].ncols + cs - 1) / cs;
-        b2 += segs[si].ncols * colb;
-      }
-    const int64_t small_fill = 12288;
-    H->geom[0] = w1 > 0 && b1 / w1 < small_fill;
-    H->geom[1] = w2 > 0 && b2 / w2 < small_fill;
-    if (getenv("HH_MV_GEOM1")) H->geom[0] = atoi(getenv("HH_MV_GEOM1")) != 0;
-    if (getenv("HH_MV_GEOM2")) H->geom[1] = atoi(getenv("HH_MV_GEOM2")) != 0;
-  }
   // Morton order (the construction order) is kept for the multi-RHS products: there z is NR
   // times larger (5.8 GB at 3D N=2^20 and 16 RHS) and leaves processed at the same time must
   // share their ancestors' z slices in L2 (ncu r02: in LPT order phase 2 at 16 RHS read 1.8x

@@ -101,8 +101,13 @@ constexpr int META = 64;
 // K range into four quarters, copies each with its own bulk copy to a shared-memory region
 // whose start is skewed by 32 B (8 banks) per quarter, and lane group kq walks quarter kq:
 // the four lanes of a fragment row then sit 8 banks apart, the eight rows fill the gaps.
+// MEASURED (profiles/r02h_ab_quart_geom.txt, r02h_proxy_nrhs16_quart_ncu.txt): the replays
+// disappear (phase-2 wavefronts 270 M -> 91 M, phase 1 172 M -> 73 M) but the kernels do not get
+// faster — phase 1 unchanged, phase 2 5-15% slower (eight bulk copies and 7% fewer columns per
+// stage, more index arithmetic): the DMMA pipe (83% / 75% issue-busy), not shared memory, is
+// the limit.  Kept as an opt-in variant; the default is the linear window.
 #ifndef HH_MV_QUART
-#define HH_MV_QUART 1
+#define HH_MV_QUART 0
 #endif
 // byte stride between the quarter regions of a stage: room for the quarter's enclosing 16-B
 // aligned window, rounded to the 128-B bank period, plus the 32-B skew
@@ -122,36 +127,20 @@ template <int NR> constexpr bool use_mma() { return HH_MV_MMA && (NR == 8 || NR 
 template <int NR, int PH> constexpr int min_ctas() { return use_mma<NR>() ? (NR == 8 && PH == 1 ? 3 : 2) : HH_MV_MINB; }
 template <int NR, int WP = 0> constexpr bool quartered() { return HH_MV_QUART && WP == 0 && use_mma<NR>(); }
 
-// GV = geometry variant, chosen per handle and phase (hh_matrix::geom): 0 = few large stages
-// (the measured winner when items fill them: 3D configs), 1 = twice the stages at half the size
-// for small-item plans (2D trees with ~16-point leaves: most windows hold < 12 KiB, so two
-// 32 KiB stages per CTA leave too few bytes in flight), NR = 1 only.
-#ifndef HH_MV_SMALL_W
-#define HH_MV_SMALL_W 16384
-#endif
-#ifndef HH_MV_SMALL_X
-#define HH_MV_SMALL_X 2048
-#endif
-#ifndef HH_MV_SMALL_STAGES
-#define HH_MV_SMALL_STAGES 4
-#endif
-template <int NR, int PH, int GV = 0> struct Geo {  // PH = phase (1: x~ rows per W row window, 2: z per U column)
-  static_assert(GV == 0 || NR == 1, "the small-item geometry is built for one RHS");
+template <int NR, int PH> struct Geo {  // PH = phase (1: x~ rows per W row window, 2: z per U column)
   // factor bytes per stage (phase 2 at NR >= 8 may use smaller stages to fit 2 CTAs/SM)
-  static constexpr int WDATA = GV == 1 ? HH_MV_SMALL_W
-                               : (PH == 2 && NR >= 16) ? HH_MV_P2HI : (PH == 1 && NR >= 16) ? HH_MV_P1HI : HH_MV_WDATA;
+  static constexpr int WDATA = (PH == 2 && NR >= 16) ? HH_MV_P2HI : (PH == 1 && NR >= 16) ? HH_MV_P1HI : HH_MV_WDATA;
   static constexpr int WBUF = WDATA + 32;                            // + 16-B alignment slack
   // vector bytes per stage: phase 1 needs one NR-vector per W row (a 248-column row is >= 1 KiB
   // of factors), phase 2 one per U column (|R| rows, as little as ~32 elements)
   static constexpr int XDATA =
-      GV == 1 ? HH_MV_SMALL_X
-      : NR <= 2 ? HH_MV_XDATA
+      NR <= 2 ? HH_MV_XDATA
               : (PH == 1 ? ((NR >= 16 && HH_MV_P1X > 0) ? HH_MV_P1X : (NR * 512 > 4096 ? NR * 512 : 4096))
                          : ((NR >= 16 && HH_MV_P2X > 0) ? HH_MV_P2X : NR * 2048 / (32768 / WDATA)));
   static constexpr int XELEMS = XDATA / 8;                        // doubles (rows x NR)
   static constexpr int XBUF = XDATA + 32;
   static constexpr int STAGE = WBUF + XBUF + META;
-  static constexpr int STAGES = GV == 1 ? HH_MV_SMALL_STAGES : (PH == 2 && NR >= 16) ? HH_MV_P2STAGES : HH_MV_STAGES;
+  static constexpr int STAGES = (PH == 2 && NR >= 16) ? HH_MV_P2STAGES : HH_MV_STAGES;
   // phase 2 at NR = 16 may reduce in the leaf's last stage (held until the reduction ends)
   static constexpr bool RED_IN_STAGE = PH == 2 && NR >= 16 && HH_MV_P2ALIAS && use_mma<NR>();
   static constexpr size_t red_bytes() {  // phase-2 cross-group reduction buffer
@@ -820,10 +809,10 @@ __device__ __forceinline__ void p1_consumer_nr1(const P1Args &a, uint8_t *smem, 
   }
 }
 
-template <int NR, int WP = 0, int GV = 0>
+template <int NR, int WP = 0>
 __global__ void __launch_bounds__(THREADS, min_ctas<NR, 1>()) k_phase1(P1Args a) {
   static_assert(WP == 0 || NR <= 4, "reduced working precision runs the FMA consumers (NR <= 4)");
-  using G = Geo<NR, 1, GV>;
+  using G = Geo<NR, 1>;
   using A = typename WpT<WP>::A;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
@@ -1313,10 +1302,10 @@ __device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, 
   }
 }
 
-template <int NR, int WP = 0, int GV = 0>
+template <int NR, int WP = 0>
 __global__ void __launch_bounds__(THREADS, min_ctas<NR, 2>()) k_phase2(P2Args a) {
   static_assert(WP == 0 || NR <= 4, "reduced working precision runs the FMA consumers (NR <= 4)");
-  using G = Geo<NR, 2, GV>;
+  using G = Geo<NR, 2>;
   using A = typename WpT<WP>::A;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
@@ -1511,11 +1500,11 @@ void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t sm
   HH_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 
-template <int NR, int WP, int GV1, int GV2>
-void matvec_chunk_g(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
+template <int NR, int WP = 0>
+void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
   using namespace mv;
-  using G1 = Geo<NR, 1, GV1>;
-  using G2 = Geo<NR, 2, GV2>;
+  using G1 = Geo<NR, 1>;
+  using G2 = Geo<NR, 2>;
   // launch geometry (device attributes, smem opt-in, occupancy) once per handle, width and
   // working precision
   hh_matrix::LaunchCfg &L = H->lcfg[WP][NR == 1 ? 0 : NR == 2 ? 1 : NR == 4 ? 2 : NR == 8 ? 3 : 4];
@@ -1523,11 +1512,11 @@ void matvec_chunk_g(hh_matrix *H, const double *x, double *y, int col0, cudaStre
     int dev = 0;
     HH_CUDA(cudaGetDevice(&dev));
     HH_CUDA(cudaDeviceGetAttribute(&L.nsm, cudaDevAttrMultiProcessorCount, dev));
-    HH_CUDA(cudaFuncSetAttribute(k_phase1<NR, WP, GV1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem(false)));
-    HH_CUDA(cudaFuncSetAttribute(k_phase2<NR, WP, GV2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::smem(true)));
+    HH_CUDA(cudaFuncSetAttribute(k_phase1<NR, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem(false)));
+    HH_CUDA(cudaFuncSetAttribute(k_phase2<NR, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::smem(true)));
     int p1 = 0, p2 = 0;
-    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_phase1<NR, WP, GV1>, THREADS, G1::smem(false)));
-    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_phase2<NR, WP, GV2>, THREADS, G2::smem(true)));
+    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_phase1<NR, WP>, THREADS, G1::smem(false)));
+    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_phase2<NR, WP>, THREADS, G2::smem(true)));
     L.grid1 = (int)std::min<int64_t>(H->n_p1_tiles, (int64_t)L.nsm * std::max(1, p1));
     L.grid2 = (int)std::min<int64_t>(H->n_p2_leaves, (int64_t)L.nsm * std::max(1, p2));
     L.ready = true;
@@ -1559,7 +1548,7 @@ void matvec_chunk_g(hh_matrix *H, const double *x, double *y, int col0, cudaStre
     a.v = v;
     a.N = H->N;
     a.ctr = ctr;
-    launch_pdl(k_phase1<NR, WP, GV1>, (unsigned)L.grid1, THREADS, G1::smem(false), st, a);
+    launch_pdl(k_phase1<NR, WP>, (unsigned)L.grid1, THREADS, G1::smem(false), st, a);
     HH_LAUNCHED();
     if (H->n_p1_comb > 0) {
       launch_pdl(k_p1_combine<NR, WP>, (unsigned)std::min<int64_t>(H->n_p1_comb, (int64_t)nsm * 8), 256, 0, st,
@@ -1581,22 +1570,10 @@ void matvec_chunk_g(hh_matrix *H, const double *x, double *y, int col0, cudaStre
   b.ldy = H->N;
   b.ctr = ctr;
   if (L.grid2 > 0) {
-    launch_pdl(k_phase2<NR, WP, GV2>, (unsigned)L.grid2, THREADS, G2::smem(true), st, b);
+    launch_pdl(k_phase2<NR, WP>, (unsigned)L.grid2, THREADS, G2::smem(true), st, b);
     HH_LAUNCHED();
   }
   mark(3);
-}
-
-// stage geometry per handle and phase (see Geo): the single-RHS fp64 product only
-template <int NR, int WP = 0>
-void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
-  if constexpr (NR == 1 && WP == 0) {
-    const int g1 = H->geom[0], g2 = H->geom[1];
-    if (g1 && g2) return matvec_chunk_g<1, 0, 1, 1>(H, x, y, col0, st);
-    if (g1) return matvec_chunk_g<1, 0, 1, 0>(H, x, y, col0, st);
-    if (g2) return matvec_chunk_g<1, 0, 0, 1>(H, x, y, col0, st);
-  }
-  matvec_chunk_g<NR, WP, 0, 0>(H, x, y, col0, st);
 }
 
 template <int WP>
