@@ -1327,6 +1327,8 @@ __global__ void __launch_bounds__(THREADS, min_ctas<NR, 2>()) k_phase2(P2Args a)
     const uint64_t pol_w = evict_first_policy(), pol_x = evict_last_policy();
     int n = 0;
     // next leaf index / descriptor and the next segment descriptor are fetched one ahead
+    // (also fetching the next leaf's first segment descriptor ahead was measured 10-25% SLOWER
+    // in phase 2 at one RHS: profiles/r02i_ab_p2prefetch.txt)
     int li = atomicAdd(a.ctr + 1, 1);
     P2Leaf Ln{};
     if (li < a.nleaves) Ln = a.leaves[li];
