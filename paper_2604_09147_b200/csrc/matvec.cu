@@ -218,6 +218,23 @@ __device__ __forceinline__ void pdl_trigger() {
 #endif
 }
 
+// Cycle probe of the NR = 1 pipelines (variant builds only, -DHH_MV_PROBE=1; the product build
+// compiles none of it): where do the producer thread and a consumer thread spend their time?
+// Slots (summed over CTAs): phase p in {1, 2} at base 8 (p - 1):
+//   +0 producer cycles in its item loop   +1 of which waiting on empty barriers   +2 stages issued
+//   +3 consumer (thread 0) cycles          +4 of which waiting on full barriers    +5 in item-end sections
+//   +6 items
+#ifndef HH_MV_PROBE
+#define HH_MV_PROBE 0
+#endif
+#if HH_MV_PROBE
+__device__ unsigned long long g_probe[16];
+__device__ __forceinline__ unsigned long long pclk() { return clock64(); }
+#define PROBE(stmt) stmt
+#else
+#define PROBE(stmt)
+#endif
+
 // Copy [src, src + bytes) as the enclosing 16-B aligned window; returns the lead offset.
 __device__ __forceinline__ int stage_copy(uint8_t *dst, const uint8_t *src, int64_t bytes, uint64_t *bar,
                                           uint64_t pol, uint32_t &tx) {
@@ -758,9 +775,12 @@ __device__ __forceinline__ void p1_consumer_nr1(const P1Args &a, uint8_t *smem, 
   int cur_ct = -1, V = 1, slots = 1, lq = 0, cs = 0, q = 0;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   int32_t zi[4] = {0, 0, 0, 0};
+  PROBE(unsigned long long ct0 = pclk(); unsigned long long cwait = 0;)
   for (int n = 0;; ++n) {
     const int s = n % G::STAGES;
+    PROBE(const unsigned long long w0 = pclk();)
     mbar_wait(&full[s], (n / G::STAGES) & 1);
+    PROBE(cwait += pclk() - w0;)
     const uint8_t *st = smem + s * G::STAGE;
     const Meta m = *reinterpret_cast<const Meta *>(st + G::WBUF + G::XBUF);
     if (m.kind) break;
@@ -807,6 +827,10 @@ __device__ __forceinline__ void p1_consumer_nr1(const P1Args &a, uint8_t *smem, 
       }
     }
   }
+  PROBE(if (tid == 0) {
+    atomicAdd(&g_probe[3], pclk() - ct0);
+    atomicAdd(&g_probe[4], cwait);
+  })
 }
 
 template <int NR, int WP = 0>
@@ -834,10 +858,12 @@ __global__ void __launch_bounds__(THREADS, min_ctas<NR, 1>()) k_phase1(P1Args a)
     int n = 0;
     // the next item index and its descriptor are requested one item ahead, so their latency
     // overlaps the current item's stage issue (small tiles are ~1 us of streaming each)
+    PROBE(unsigned long long pt0 = pclk(); unsigned long long pwait = 0; unsigned long long pitems = 0;)
     int item = atomicAdd(a.ctr, 1);
     P1Tile Tn{};
     if (item < a.ntiles) Tn = a.tiles[item];
     while (item < a.ntiles) {
+      PROBE(++pitems;)
       const P1Tile T = Tn;
       const int nxt = atomicAdd(a.ctr, 1);
       if (nxt < a.ntiles) Tn = a.tiles[nxt];
@@ -854,7 +880,9 @@ __global__ void __launch_bounds__(THREADS, min_ctas<NR, 1>()) k_phase1(P1Args a)
       for (int r0 = 0; r0 < T.n; r0 += rs, ++n) {
         const int r1 = min(T.n, r0 + rs);
         const int s = n % G::STAGES;
+        PROBE(const unsigned long long w0 = pclk();)
         if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
+        PROBE(pwait += pclk() - w0;)
         uint8_t *st = smem + s * G::STAGE;
         const uint8_t *wsrc = wbase + (int64_t)r0 * rowb;
         const int64_t wlen = (int64_t)(r1 - r0) * rowb;
@@ -897,6 +925,12 @@ __global__ void __launch_bounds__(THREADS, min_ctas<NR, 1>()) k_phase1(P1Args a)
       }
       item = nxt;
     }
+    PROBE(if (NR == 1 && WP == 0) {
+      atomicAdd(&g_probe[0], pclk() - pt0);
+      atomicAdd(&g_probe[1], pwait);
+      atomicAdd(&g_probe[2], (unsigned long long)n);
+      atomicAdd(&g_probe[6], pitems);
+    })
     const int s = n % G::STAGES;
     if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
     reinterpret_cast<Meta *>(smem + s * G::STAGE + G::WBUF + G::XBUF)->kind = 1;
@@ -1216,9 +1250,12 @@ __device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, 
   int64_t cur_leaf = -1, yi = 0;                 // the leaf's first tree position, y index of row rr
   int64_t ys[4] = {0, 0, 0, 0};                  // (HH_MV_P2RED = 0) y indices of this slot's rows
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  PROBE(unsigned long long ct0 = pclk(); unsigned long long cwait = 0; unsigned long long cend = 0;)
   for (int n = 0;; ++n) {
     const int s = n % G::STAGES;
+    PROBE(const unsigned long long w0 = pclk();)
     mbar_wait(&full[s], (n / G::STAGES) & 1);
+    PROBE(cwait += pclk() - w0;)
     uint8_t *st = smem + s * G::STAGE;
     const Meta m = *reinterpret_cast<const Meta *>(st + G::WBUF + G::XBUF);
     if (m.kind) break;
@@ -1265,6 +1302,7 @@ __device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, 
       continue;
     }
     // last window of the leaf: fixed-order reduction over the Gn groups in this stage's data
+    PROBE(const unsigned long long e0 = pclk();)
     consumer_sync();  // every warp is done with the stage's U / z
     double *red = reinterpret_cast<double *>(st);
 #pragma unroll
@@ -1299,7 +1337,13 @@ __device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, 
       for (int i = 0; i < 4; ++i)
         if (i < V) a.y[ys[i]] = sv[i];
 #endif
+    PROBE(cend += pclk() - e0;)
   }
+  PROBE(if (tid == 0) {
+    atomicAdd(&g_probe[11], pclk() - ct0);
+    atomicAdd(&g_probe[12], cwait);
+    atomicAdd(&g_probe[13], cend);
+  })
 }
 
 template <int NR, int WP = 0>
@@ -1329,10 +1373,12 @@ __global__ void __launch_bounds__(THREADS, min_ctas<NR, 2>()) k_phase2(P2Args a)
     // next leaf index / descriptor and the next segment descriptor are fetched one ahead
     // (also fetching the next leaf's first segment descriptor ahead was measured 10-25% SLOWER
     // in phase 2 at one RHS: profiles/r02i_ab_p2prefetch.txt)
+    PROBE(unsigned long long pt0 = pclk(); unsigned long long pwait = 0; unsigned long long pitems = 0;)
     int li = atomicAdd(a.ctr + 1, 1);
     P2Leaf Ln{};
     if (li < a.nleaves) Ln = a.leaves[li];
     while (li < a.nleaves) {
+      PROBE(++pitems;)
       const P2Leaf Lf = Ln;
       const int nxt = atomicAdd(a.ctr + 1, 1);
       if (nxt < a.nleaves) Ln = a.leaves[nxt];
@@ -1353,7 +1399,9 @@ __global__ void __launch_bounds__(THREADS, min_ctas<NR, 2>()) k_phase2(P2Args a)
         for (int c0 = 0; c0 < S.ncols; c0 += cs, ++n) {
           const int c1 = min(S.ncols, c0 + cs);
           const int s = n % G::STAGES;
+          PROBE(const unsigned long long w0 = pclk();)
           if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
+          PROBE(pwait += pclk() - w0;)
           uint8_t *st = smem + s * G::STAGE;
           const uint8_t *usrc = ubase + (int64_t)c0 * colb;
           const int64_t ulen = (int64_t)(c1 - c0) * colb;
@@ -1396,6 +1444,12 @@ __global__ void __launch_bounds__(THREADS, min_ctas<NR, 2>()) k_phase2(P2Args a)
       }
       li = nxt;
     }
+    PROBE(if (NR == 1 && WP == 0) {
+      atomicAdd(&g_probe[8], pclk() - pt0);
+      atomicAdd(&g_probe[9], pwait);
+      atomicAdd(&g_probe[10], (unsigned long long)n);
+      atomicAdd(&g_probe[14], pitems);
+    })
     const int s = n % G::STAGES;
     if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
     reinterpret_cast<Meta *>(smem + s * G::STAGE + G::WBUF + G::XBUF)->kind = 1;
@@ -1596,6 +1650,20 @@ void run_matvec_wp(hh_matrix *H, const double *x, double *y, int nrhs, cudaStrea
     }
   }
 }
+
+#if HH_MV_PROBE
+}  // namespace hh
+// variant builds only: read (and optionally reset) the cycle probe
+extern "C" int hh_debug_probe(unsigned long long *out, int reset) {
+  if (out && cudaMemcpyFromSymbol(out, hh::mv::g_probe, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+  if (reset) {
+    unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(hh::mv::g_probe, z, sizeof(z)) != cudaSuccess) return 1;
+  }
+  return 0;
+}
+namespace hh {
+#endif
 
 void run_matvec(hh_matrix *H, const double *x, double *y, int nrhs, cudaStream_t st, int wp) {
   if (wp == 1) return run_matvec_wp<1>(H, x, y, nrhs, st);
