@@ -267,6 +267,18 @@ hh_status hh_build(const double *points, int64_t N, int32_t d, hh_kernel kernel,
       H->n_p1_tiles = (int64_t)tiles.size();
       H->n_p2_leaves = (int64_t)leaves.size();
       H->v.alloc(sizeof(double) * 16 * (size_t)(N + H->ztotal) + 64);
+      {  // stage plan of the single-RHS product (absolute addresses: arenas and v exist now)
+        std::vector<StageItem> sitem[2];
+        std::vector<StageCopy> scopy[2];
+        std::vector<StageMeta> smeta[2];
+        build_stage_plan(H, tiles, segs, leaves, sitem, scopy, smeta);
+        for (int ph = 0; ph < 2; ++ph) {
+          h2d(H->st_item[ph], sitem[ph], st);
+          h2d(H->st_copy[ph], scopy[ph], st);
+          h2d(H->st_meta[ph], smeta[ph], st);
+        }
+        HH_CUDA(cudaStreamSynchronize(st));  // the host vectors go out of scope
+      }
       H->ctr.alloc(64);
       HH_CUDA(cudaMemsetAsync(H->ctr.p, 0, 64, st));
       HH_CUDA(cudaStreamSynchronize(st));

@@ -55,6 +55,11 @@ void cluster_range(const hh_matrix *H, int l, int64_t m, int64_t &a, int64_t &n)
 void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &zmap, std::vector<P1Combine> &comb,
                 int64_t &npartial, std::vector<P2Seg> &segs, std::vector<P2Leaf> &leaves,
                 std::vector<P2Leaf> &leaves_morton);
+// Stage plan of the single-RHS product (handle.h StageMeta / StageCopy): needs the arenas and
+// the workspace H->v allocated (absolute device addresses); chooses H->geom per phase.
+void build_stage_plan(hh_matrix *H, const std::vector<P1Tile> &tiles, const std::vector<P2Seg> &segs,
+                      const std::vector<P2Leaf> &leaves, std::vector<StageItem> (&item)[2],
+                      std::vector<StageCopy> (&copy)[2], std::vector<StageMeta> (&meta)[2]);
 void run_matvec(hh_matrix *H, const double *x, double *y, int nrhs, cudaStream_t st, int wp = 0);
 void print_build_profile();
 

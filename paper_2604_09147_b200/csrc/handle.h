@@ -76,6 +76,43 @@ struct P2Leaf {
   int64_t s0, s1;     // segments [s0, s1)
 };
 
+// Stage plan of the single-RHS product: every shared-memory stage the
+// persistent kernels will stream — one window of a W tile (phase 1) or of a leaf's U / dense
+// segment (phase 2) with its vector slice — is precomputed at build time: the two bulk-copy
+// windows (StageCopy) and the descriptor the consumers read (StageMeta).  The producer thread
+// then only waits for a free stage and issues three bulk copies (factor window, vector window,
+// descriptor); computing the windows on the fly cost it ~250 dependent instructions per stage,
+// which bounded the small-leaf workloads (2D: ~7 KiB per stage).
+struct StageMeta {     // 64 B, read by the consumers from the stage's descriptor slot
+  int32_t kind;        // 0 = work, 1 = end of stream
+  int32_t wlead;       // bytes between the staged window start and element 0
+  int32_t xlead;
+  int32_t r0, r1;      // phase 1: rows [r0, r1) of the tile;  phase 2: columns [r0, r1) of the segment
+  int32_t flags;       // phase 2: bit 0 = last stage of the leaf
+  int32_t a, b;        // phase 1: ct, tag;  phase 2: nr, tag | dense << 8
+  int64_t p, q;        // phase 1: zbase, rows of the piece;  phase 2: leaf r0, -
+  int64_t pb;          // phase 1: partial index of column 0 (row-split tile) or -1
+  int64_t pad;
+};
+static_assert(sizeof(StageMeta) == 64, "stage descriptor slot");
+struct StageCopy {     // 32 B: 16-B aligned enclosing windows (bytes may be 0: no copy)
+  uint64_t wsrc, xsrc;
+  uint32_t wbytes, xbytes;
+  uint32_t pad[2];
+};
+static_assert(sizeof(StageCopy) == 32, "stage copy record");
+struct StageItem {     // 48 B: an item's stages [s0, s1) and its first copy record (no dependent load)
+  int64_t s0, s1;
+  StageCopy first;
+};
+static_assert(sizeof(StageItem) == 48, "stage item record");
+// single-RHS stage geometries (matvec.cu Geo<1, PH, GV>): factor bytes, vector entries, ring depth.
+// GV 1 (twice the stages at half the size) serves plans whose windows are mostly small.
+struct StageGeo {
+  int wdata, xelems, stages;
+};
+constexpr StageGeo kStageGeo[2] = {{32768, 512, 2}, {16384, 256, 4}};
+
 }  // namespace hh
 
 struct hh_matrix {
@@ -108,6 +145,10 @@ struct hh_matrix {
   // matvec plan
   hh::DBuf p1_tiles, zmap, p2_segs, p2_leaves, p2_leaves_mo, p1_comb, partial;  // leaves: LPT / Morton order
   int64_t n_p1_tiles = 0, n_p2_leaves = 0, n_p1_comb = 0, n_partial = 0;
+  // stage plan of the single-RHS product: per phase the items' stage ranges (item order), copy
+  // records and descriptors; geom = stage geometry per phase (kStageGeo index)
+  hh::DBuf st_item[2], st_copy[2], st_meta[2];
+  int geom[2] = {0, 0};
   hh::DBuf v;        // [(N + ztotal) * 16] doubles (+ slack for 16-B aligned superset copies)
   hh::DBuf ctr;      // work counters of the persistent matvec kernels (zeroed by the gather)
   struct LaunchCfg {  // per RHS-chunk width (1, 2, 4, 8, 16): set once, reused by every hh_matvec

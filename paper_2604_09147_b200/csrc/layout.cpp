@@ -416,4 +416,107 @@ void build_plan(hh_matrix *H, std::vector<P1Tile> &tiles, std::vector<int32_t> &
 #endif
 }
 
+// ----------------------------------------------------------------- single-RHS stage plan
+// The windows are exactly those the on-the-fly producer of matvec.cu would form for NR = 1
+// (rows per stage = min(vector entries, factor bytes / row bytes), at least 1), so the
+// consumers see the same descriptors either way.
+namespace {
+void add_stage(std::vector<StageCopy> &copy, std::vector<StageMeta> &meta, uint64_t wsrc, int64_t wlen, uint64_t xsrc,
+               int64_t xlen, StageMeta m) {
+  auto win = [](uint64_t s, int64_t len, uint64_t &a, uint32_t &bytes) {
+    a = s & ~(uint64_t)15;
+    bytes = len > 0 ? (uint32_t)(((s + (uint64_t)len + 15) & ~(uint64_t)15) - a) : 0u;
+  };
+  StageCopy c{};
+  win(wsrc, wlen, c.wsrc, c.wbytes);
+  win(xsrc, xlen, c.xsrc, c.xbytes);
+  m.kind = 0;
+  m.wlead = (int32_t)(wsrc & 15);
+  m.xlead = (int32_t)(xsrc & 15);
+  copy.push_back(c);
+  meta.push_back(m);
+}
+}  // namespace
+
+void build_stage_plan(hh_matrix *H, const std::vector<P1Tile> &tiles, const std::vector<P2Seg> &segs,
+                      const std::vector<P2Leaf> &leaves, std::vector<StageItem> (&item)[2],
+                      std::vector<StageCopy> (&copy)[2], std::vector<StageMeta> (&meta)[2]) {
+  const uint64_t vaddr = (uint64_t)(uintptr_t)H->v.p;
+  // Stage geometry per phase: kStageGeo[0] everywhere.  The deeper ring of smaller stages
+  // (kStageGeo[1]) was measured slower on every workload, small-leaf plans included
+  // (profiles/r02h_ab_quart_geom.txt, r02k_ab_planned.txt): those are bound by per-stage
+  // instruction overhead in the consumers, which more and smaller stages only multiply.
+  // HH_MV_GEOM1 / HH_MV_GEOM2 = 1 select it per phase for A/B runs.
+  H->geom[0] = getenv("HH_MV_GEOM1") ? atoi(getenv("HH_MV_GEOM1")) != 0 : 0;
+  H->geom[1] = getenv("HH_MV_GEOM2") ? atoi(getenv("HH_MV_GEOM2")) != 0 : 0;
+  for (int ph = 0; ph < 2; ++ph) {
+    item[ph].clear();
+    copy[ph].clear();
+    meta[ph].clear();
+  }
+  auto close_item = [&](int ph, int64_t s0) {
+    StageItem it{};
+    it.s0 = s0;
+    it.s1 = (int64_t)copy[ph].size();
+    if (it.s1 > it.s0) it.first = copy[ph][s0];
+    item[ph].push_back(it);
+  };
+  // ---- phase 1: tile windows of rs rows
+  {
+    const StageGeo g = kStageGeo[H->geom[0]];
+    item[0].reserve(tiles.size());
+    for (const P1Tile &T : tiles) {
+      const int64_t first = (int64_t)copy[0].size();
+      const int w = tag_bytes(T.tag);
+      const int64_t rowb = (int64_t)T.ct * w;
+      const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(g.xelems, g.wdata / rowb));
+      const uint64_t wbase = (uint64_t)(uintptr_t)H->W[T.tag].p + (uint64_t)T.src + (uint64_t)T.r0 * rowb;
+      const uint64_t xbase = vaddr + (uint64_t)(T.x0 + T.r0) * 8;
+      for (int64_t r0 = 0; r0 < T.n; r0 += rs) {
+        const int64_t r1 = std::min<int64_t>(T.n, r0 + rs);
+        StageMeta m{};
+        m.r0 = (int32_t)r0;
+        m.r1 = (int32_t)r1;
+        m.a = T.ct;
+        m.b = T.tag;
+        m.p = T.zbase;
+        m.q = T.n;
+        m.pb = T.pbase;
+        add_stage(copy[0], meta[0], wbase + (uint64_t)r0 * rowb, (r1 - r0) * rowb, xbase + (uint64_t)r0 * 8,
+                  (r1 - r0) * 8, m);
+      }
+      close_item(0, first);
+    }
+  }
+  // ---- phase 2: segment windows of cs columns, leaves in the order of `leaves`
+  {
+    const StageGeo g = kStageGeo[H->geom[1]];
+    item[1].reserve(leaves.size());
+    for (const P2Leaf &lf : leaves) {
+      const int64_t first = (int64_t)copy[1].size();
+      for (int64_t si = lf.s0; si < lf.s1; ++si) {
+        const P2Seg &S = segs[si];
+        const int w = tag_bytes(S.tag);
+        const int64_t colb = (int64_t)lf.nr * w;
+        const int64_t cs = std::max<int64_t>(1, std::min<int64_t>(g.xelems, g.wdata / colb));
+        const uint64_t ubase = (uint64_t)(uintptr_t)(S.dense ? H->D.p : H->U[S.tag].p) + (uint64_t)S.src;
+        const uint64_t zbase = vaddr + (uint64_t)S.vbeg * 8;
+        for (int64_t c0 = 0; c0 < S.ncols; c0 += cs) {
+          const int64_t c1 = std::min<int64_t>(S.ncols, c0 + cs);
+          StageMeta m{};
+          m.r0 = (int32_t)c0;
+          m.r1 = (int32_t)c1;
+          m.flags = (si + 1 == lf.s1 && c1 == S.ncols) ? 1 : 0;
+          m.a = lf.nr;
+          m.b = S.tag | (S.dense << 8);
+          m.p = lf.r0;
+          add_stage(copy[1], meta[1], ubase + (uint64_t)c0 * colb, (c1 - c0) * colb, zbase + (uint64_t)c0 * 8,
+                    (c1 - c0) * 8, m);
+        }
+      }
+      close_item(1, first);
+    }
+  }
+}
+
 }  // namespace hh

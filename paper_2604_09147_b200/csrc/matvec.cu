@@ -127,20 +127,33 @@ template <int NR> constexpr bool use_mma() { return HH_MV_MMA && (NR == 8 || NR 
 template <int NR, int PH> constexpr int min_ctas() { return use_mma<NR>() ? (NR == 8 && PH == 1 ? 3 : 2) : HH_MV_MINB; }
 template <int NR, int WP = 0> constexpr bool quartered() { return HH_MV_QUART && WP == 0 && use_mma<NR>(); }
 
-template <int NR, int PH> struct Geo {  // PH = phase (1: x~ rows per W row window, 2: z per U column)
+// Precomputed stage plan for the single-RHS fp64 product (handle.h StageCopy / StageMeta /
+// StageItem; built by layout.cpp build_stage_plan): the producer only issues copies.  0 = the
+// on-the-fly producer at NR = 1 too (variant builds, A/B).
+#ifndef HH_MV_DESC
+#define HH_MV_DESC 1
+#endif
+template <int NR, int WP = 0> constexpr bool planned() { return HH_MV_DESC && NR == 1 && WP == 0; }
+
+// GV = stage geometry variant of the planned product (kStageGeo[GV], chosen per handle and phase)
+template <int NR, int PH, int GV = 0> struct Geo {  // PH = phase (1: x~ rows per W row window, 2: z per U column)
+  static_assert(GV == 0 || (NR == 1 && HH_MV_DESC), "geometry variants belong to the planned single-RHS product");
   // factor bytes per stage (phase 2 at NR >= 8 may use smaller stages to fit 2 CTAs/SM)
-  static constexpr int WDATA = (PH == 2 && NR >= 16) ? HH_MV_P2HI : (PH == 1 && NR >= 16) ? HH_MV_P1HI : HH_MV_WDATA;
+  static constexpr int WDATA = (NR == 1 && HH_MV_DESC) ? kStageGeo[GV].wdata
+                               : (PH == 2 && NR >= 16) ? HH_MV_P2HI : (PH == 1 && NR >= 16) ? HH_MV_P1HI : HH_MV_WDATA;
   static constexpr int WBUF = WDATA + 32;                            // + 16-B alignment slack
   // vector bytes per stage: phase 1 needs one NR-vector per W row (a 248-column row is >= 1 KiB
   // of factors), phase 2 one per U column (|R| rows, as little as ~32 elements)
   static constexpr int XDATA =
-      NR <= 2 ? HH_MV_XDATA
+      (NR == 1 && HH_MV_DESC) ? kStageGeo[GV].xelems * 8
+      : NR <= 2 ? HH_MV_XDATA
               : (PH == 1 ? ((NR >= 16 && HH_MV_P1X > 0) ? HH_MV_P1X : (NR * 512 > 4096 ? NR * 512 : 4096))
                          : ((NR >= 16 && HH_MV_P2X > 0) ? HH_MV_P2X : NR * 2048 / (32768 / WDATA)));
   static constexpr int XELEMS = XDATA / 8;                        // doubles (rows x NR)
   static constexpr int XBUF = XDATA + 32;
   static constexpr int STAGE = WBUF + XBUF + META;
-  static constexpr int STAGES = (PH == 2 && NR >= 16) ? HH_MV_P2STAGES : HH_MV_STAGES;
+  static constexpr int STAGES = (NR == 1 && HH_MV_DESC) ? kStageGeo[GV].stages
+                                : (PH == 2 && NR >= 16) ? HH_MV_P2STAGES : HH_MV_STAGES;
   // phase 2 at NR = 16 may reduce in the leaf's last stage (held until the reduction ends)
   static constexpr bool RED_IN_STAGE = PH == 2 && NR >= 16 && HH_MV_P2ALIAS && use_mma<NR>();
   static constexpr size_t red_bytes() {  // phase-2 cross-group reduction buffer
@@ -151,17 +164,9 @@ template <int NR, int PH> struct Geo {  // PH = phase (1: x~ rows per W row wind
   }
 };
 
-// Stage descriptor written by the producer before it arrives on the stage's full barrier.
-struct Meta {
-  int32_t kind;      // 0 = work, 1 = end of stream
-  int32_t wlead;     // bytes between the staged window start and element 0
-  int32_t xlead;
-  int32_t r0, r1;    // phase 1: rows [r0, r1) of the tile;  phase 2: columns [r0, r1) of the segment
-  int32_t flags;     // phase 2: bit 0 = last stage of the leaf
-  int32_t a, b;      // phase 1: ct, tag;  phase 2: nr, tag | dense << 8
-  int64_t p, q;      // phase 1: zbase, rows of the piece;  phase 2: leaf r0, -
-  int64_t pb;        // phase 1: partial index of column 0 (row-split tile) or -1
-};
+// Stage descriptor the consumers read from the stage's last 64 bytes (handle.h StageMeta):
+// written by the producer thread, or delivered by a bulk copy from the precomputed stage plan.
+using Meta = StageMeta;
 static_assert(sizeof(Meta) <= META, "meta");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -331,6 +336,74 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Producer of the planned single-RHS product: items from the work counter, for every stage of
+// the item three bulk copies (factor window, vector window, 64-B descriptor) completing on the
+// stage's full barrier.  The next item record and the next copy record are loaded one ahead.
+struct PlanArgs {
+  const StageItem *items;
+  const StageCopy *copies;
+  const StageMeta *metas;
+};
+__device__ __forceinline__ StageCopy load_copy(const StageCopy *p) {
+  const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p)), b = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
+  StageCopy c;
+  c.wsrc = (uint64_t)a.x | ((uint64_t)a.y << 32);
+  c.xsrc = (uint64_t)a.z | ((uint64_t)a.w << 32);
+  c.wbytes = b.x;
+  c.xbytes = b.y;
+  return c;
+}
+template <class G, int PH>
+__device__ __forceinline__ void planned_producer(const PlanArgs &pl, int64_t nitems, int *ctr, uint8_t *smem,
+                                                 uint64_t *full, uint64_t *empty) {
+  const uint64_t pol_w = evict_first_policy(), pol_x = evict_last_policy();
+  int n = 0;
+  PROBE(unsigned long long pt0 = pclk(); unsigned long long pwait = 0; unsigned long long pitems = 0;)
+  int item = atomicAdd(ctr, 1);
+  int64_t s0n = 0, s1n = 0;
+  StageCopy cn{};
+  if (item < nitems) {
+    const uint4 r = __ldg(reinterpret_cast<const uint4 *>(pl.items + item));
+    s0n = (int64_t)((uint64_t)r.x | ((uint64_t)r.y << 32));
+    s1n = (int64_t)((uint64_t)r.z | ((uint64_t)r.w << 32));
+    cn = load_copy(&pl.items[item].first);
+  }
+  while (item < nitems) {
+    const int64_t s0 = s0n, s1 = s1n;
+    StageCopy c = cn;
+    const int nxt = atomicAdd(ctr, 1);
+    if (nxt < nitems) {
+      const uint4 r = __ldg(reinterpret_cast<const uint4 *>(pl.items + nxt));
+      s0n = (int64_t)((uint64_t)r.x | ((uint64_t)r.y << 32));
+      s1n = (int64_t)((uint64_t)r.z | ((uint64_t)r.w << 32));
+      cn = load_copy(&pl.items[nxt].first);
+    }
+    StageCopy c1{};
+    if (s0 + 1 < s1) c1 = load_copy(pl.copies + s0 + 1);
+    PROBE(++pitems;)
+    for (int64_t si = s0; si < s1; ++si, ++n) {
+      const int s = n % G::STAGES;
+      PROBE(const unsigned long long w0 = pclk();)
+      if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
+      PROBE(pwait += pclk() - w0;)
+      uint8_t *st = smem + s * G::STAGE;
+      mbar_expect_tx(&full[s], c.wbytes + c.xbytes + (uint32_t)sizeof(StageMeta));
+      if (c.wbytes) bulk_g2s(st, reinterpret_cast<const void *>(c.wsrc), c.wbytes, &full[s], pol_w);
+      if (c.xbytes) bulk_g2s(st + G::WBUF, reinterpret_cast<const void *>(c.xsrc), c.xbytes, &full[s], pol_x);
+      bulk_g2s(st + G::WBUF + G::XBUF, pl.metas + si, (uint32_t)sizeof(StageMeta), &full[s], pol_w);
+      c = c1;
+      if (si + 2 < s1) c1 = load_copy(pl.copies + si + 2);
+    }
+    item = nxt;
+  }
+  PROBE(atomicAdd(&g_probe[8 * (PH - 1)], pclk() - pt0); atomicAdd(&g_probe[8 * (PH - 1) + 1], pwait);
+        atomicAdd(&g_probe[8 * (PH - 1) + 2], (unsigned long long)n); atomicAdd(&g_probe[8 * (PH - 1) + 6], pitems);)
+  const int s = n % G::STAGES;
+  if (n >= G::STAGES) mbar_wait(&empty[s], ((n / G::STAGES) & 1) ^ 1);
+  reinterpret_cast<Meta *>(smem + s * G::STAGE + G::WBUF + G::XBUF)->kind = 1;
+  mbar_arrive(&full[s]);
+}
+
 // --------------------------------------------------------------------------- working precision
 // Alg. 3 "compute in working precision u" with u below fp64 — the paper's
 // backward-error study (Thm 4.4).  Reading G27: x and every
@@ -441,6 +514,7 @@ struct P1Args {
   double *v;          // [x~ (N) ; z] x NR
   int64_t N;
   int *ctr;
+  PlanArgs plan;      // planned single-RHS product only
 };
 
 // Register blocking: at NR >= 8 each thread owns MB = 2 factor columns (phase 1) or rows
@@ -740,12 +814,15 @@ __device__ __forceinline__ void loadv(const typename Elem<TAG>::T *e, double (&w
   }
 }
 
-// acc[i] += w(row j, element i) * v[j] over the cnt rows this thread owns (V chains)
+// acc[i] += w(row j, element i) * v[j] over the rows j = j0, j0 + jstep, ... < jend this thread
+// owns (V chains; e / v point at row j0).  The bound is tested on j itself: no per-stage
+// integer division for the trip count (the small-leaf workloads are issue-bound on exactly
+// this kind of per-stage overhead, profiles/r02k_probe.txt)
 template <int TAG, int V>
-__device__ __forceinline__ void vec_acc(const typename Elem<TAG>::T *e, const double *v, int cnt, int es, int vs,
-                                        double (&acc)[4]) {
+__device__ __forceinline__ void vec_acc(const typename Elem<TAG>::T *e, const double *v, int j0, int jend, int jstep,
+                                        int es, int vs, double (&acc)[4]) {
 #pragma unroll 2
-  for (int j = 0; j < cnt; ++j) {
+  for (int j = j0; j < jend; j += jstep) {
     double w[V];
     loadv<TAG, V>(e, w);
     const double x = *v;
@@ -757,11 +834,11 @@ __device__ __forceinline__ void vec_acc(const typename Elem<TAG>::T *e, const do
 }
 
 template <int V>
-__device__ __forceinline__ void vec_acc_tag(int tag, const uint8_t *base, int e0, const double *v, int cnt, int es,
-                                            int vs, double (&acc)[4]) {
+__device__ __forceinline__ void vec_acc_tag(int tag, const uint8_t *base, int e0, const double *v, int j0, int jend,
+                                            int jstep, int es, int vs, double (&acc)[4]) {
   dispatch_tag(tag, [&](auto t) {
     constexpr int TG = decltype(t)::value;
-    vec_acc<TG, V>(reinterpret_cast<const typename Elem<TG>::T *>(base) + e0, v, cnt, es, vs, acc);
+    vec_acc<TG, V>(reinterpret_cast<const typename Elem<TG>::T *>(base) + e0, v, j0, jend, jstep, es, vs, acc);
   });
 }
 
@@ -807,9 +884,8 @@ __device__ __forceinline__ void p1_consumer_nr1(const P1Args &a, uint8_t *smem, 
       const uint8_t *wst = st + m.wlead;
       const double *xst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
       const int nrows = m.r1 - m.r0;
-      const int cnt = q < nrows ? (nrows - q + Q - 1) / Q : 0;
-      if (V == 4) vec_acc_tag<4>(m.b, wst, q * ct + 4 * cs, xst + q, cnt, Q * ct, Q, acc);
-      else vec_acc_tag<1>(m.b, wst, q * ct + cs, xst + q, cnt, Q * ct, Q, acc);
+      if (V == 4) vec_acc_tag<4>(m.b, wst, q * ct + 4 * cs, xst + q, q, nrows, Q, Q * ct, Q, acc);
+      else vec_acc_tag<1>(m.b, wst, q * ct + cs, xst + q, q, nrows, Q, Q * ct, Q, acc);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -833,10 +909,10 @@ __device__ __forceinline__ void p1_consumer_nr1(const P1Args &a, uint8_t *smem, 
   })
 }
 
-template <int NR, int WP = 0>
+template <int NR, int WP = 0, int GV = 0>
 __global__ void __launch_bounds__(THREADS, min_ctas<NR, 1>()) k_phase1(P1Args a) {
   static_assert(WP == 0 || NR <= 4, "reduced working precision runs the FMA consumers (NR <= 4)");
-  using G = Geo<NR, 1>;
+  using G = Geo<NR, 1, GV>;
   using A = typename WpT<WP>::A;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
@@ -854,6 +930,10 @@ __global__ void __launch_bounds__(THREADS, min_ctas<NR, 1>()) k_phase1(P1Args a)
   pdl_trigger();
   if (warp == NCW) {  // ------------------------------------------------ producer
     if (lane != 0) return;
+    if constexpr (planned<NR, WP>()) {
+      planned_producer<G, 1>(a.plan, a.ntiles, a.ctr, smem, full, empty);
+      return;
+    }
     const uint64_t pol_w = evict_first_policy(), pol_x = evict_last_policy();
     int n = 0;
     // the next item index and its descriptor are requested one item ahead, so their latency
@@ -1025,6 +1105,7 @@ struct P2Args {
   double *y;
   int64_t ldy;
   int *ctr;
+  PlanArgs plan;      // planned single-RHS product only
 };
 
 // Phase-2 DMMA consumer (NR = 8, 16): the leaf's rows form ceil(nr/8) M-tiles, grouped by
@@ -1290,11 +1371,10 @@ __device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, 
       const uint8_t *ust = st + m.wlead;
       const double *zst = reinterpret_cast<const double *>(st + G::WBUF + m.xlead);
       const int ncols = m.r1 - m.r0;
-      const int cnt = g < ncols ? (ncols - g + Gn - 1) / Gn : 0;
       const int e0 = g * nr + rs * V;
-      if (V == 4) vec_acc_tag<4>(m.b & 0xff, ust, e0, zst + g, cnt, Gn * nr, Gn, acc);
-      else if (V == 2) vec_acc_tag<2>(m.b & 0xff, ust, e0, zst + g, cnt, Gn * nr, Gn, acc);
-      else vec_acc_tag<1>(m.b & 0xff, ust, e0, zst + g, cnt, Gn * nr, Gn, acc);
+      if (V == 4) vec_acc_tag<4>(m.b & 0xff, ust, e0, zst + g, g, ncols, Gn, Gn * nr, Gn, acc);
+      else if (V == 2) vec_acc_tag<2>(m.b & 0xff, ust, e0, zst + g, g, ncols, Gn, Gn * nr, Gn, acc);
+      else vec_acc_tag<1>(m.b & 0xff, ust, e0, zst + g, g, ncols, Gn, Gn * nr, Gn, acc);
     }
     __syncwarp();
     if (!(m.flags & 1)) {
@@ -1346,10 +1426,10 @@ __device__ __forceinline__ void p2_consumer_nr1(const P2Args &a, uint8_t *smem, 
   })
 }
 
-template <int NR, int WP = 0>
+template <int NR, int WP = 0, int GV = 0>
 __global__ void __launch_bounds__(THREADS, min_ctas<NR, 2>()) k_phase2(P2Args a) {
   static_assert(WP == 0 || NR <= 4, "reduced working precision runs the FMA consumers (NR <= 4)");
-  using G = Geo<NR, 2>;
+  using G = Geo<NR, 2, GV>;
   using A = typename WpT<WP>::A;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::STAGES * G::STAGE);
@@ -1368,6 +1448,10 @@ __global__ void __launch_bounds__(THREADS, min_ctas<NR, 2>()) k_phase2(P2Args a)
   pdl_trigger();
   if (warp == NCW) {  // ------------------------------------------------ producer
     if (lane != 0) return;
+    if constexpr (planned<NR, WP>()) {
+      planned_producer<G, 2>(a.plan, a.nleaves, a.ctr + 1, smem, full, empty);
+      return;
+    }
     const uint64_t pol_w = evict_first_policy(), pol_x = evict_last_policy();
     int n = 0;
     // next leaf index / descriptor and the next segment descriptor are fetched one ahead
@@ -1556,11 +1640,11 @@ void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t sm
   HH_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 
-template <int NR, int WP = 0>
-void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
+template <int NR, int WP, int GV1, int GV2>
+void matvec_chunk_g(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
   using namespace mv;
-  using G1 = Geo<NR, 1>;
-  using G2 = Geo<NR, 2>;
+  using G1 = Geo<NR, 1, GV1>;
+  using G2 = Geo<NR, 2, GV2>;
   // launch geometry (device attributes, smem opt-in, occupancy) once per handle, width and
   // working precision
   hh_matrix::LaunchCfg &L = H->lcfg[WP][NR == 1 ? 0 : NR == 2 ? 1 : NR == 4 ? 2 : NR == 8 ? 3 : 4];
@@ -1568,11 +1652,11 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     int dev = 0;
     HH_CUDA(cudaGetDevice(&dev));
     HH_CUDA(cudaDeviceGetAttribute(&L.nsm, cudaDevAttrMultiProcessorCount, dev));
-    HH_CUDA(cudaFuncSetAttribute(k_phase1<NR, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem(false)));
-    HH_CUDA(cudaFuncSetAttribute(k_phase2<NR, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::smem(true)));
+    HH_CUDA(cudaFuncSetAttribute(k_phase1<NR, WP, GV1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem(false)));
+    HH_CUDA(cudaFuncSetAttribute(k_phase2<NR, WP, GV2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::smem(true)));
     int p1 = 0, p2 = 0;
-    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_phase1<NR, WP>, THREADS, G1::smem(false)));
-    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_phase2<NR, WP>, THREADS, G2::smem(true)));
+    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_phase1<NR, WP, GV1>, THREADS, G1::smem(false)));
+    HH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_phase2<NR, WP, GV2>, THREADS, G2::smem(true)));
     L.grid1 = (int)std::min<int64_t>(H->n_p1_tiles, (int64_t)L.nsm * std::max(1, p1));
     L.grid2 = (int)std::min<int64_t>(H->n_p2_leaves, (int64_t)L.nsm * std::max(1, p2));
     L.ready = true;
@@ -1604,7 +1688,8 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
     a.v = v;
     a.N = H->N;
     a.ctr = ctr;
-    launch_pdl(k_phase1<NR, WP>, (unsigned)L.grid1, THREADS, G1::smem(false), st, a);
+    a.plan = PlanArgs{H->st_item[0].as<StageItem>(), H->st_copy[0].as<StageCopy>(), H->st_meta[0].as<StageMeta>()};
+    launch_pdl(k_phase1<NR, WP, GV1>, (unsigned)L.grid1, THREADS, G1::smem(false), st, a);
     HH_LAUNCHED();
     if (H->n_p1_comb > 0) {
       launch_pdl(k_p1_combine<NR, WP>, (unsigned)std::min<int64_t>(H->n_p1_comb, (int64_t)nsm * 8), 256, 0, st,
@@ -1625,11 +1710,24 @@ void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream
   b.y = y + (int64_t)col0 * H->N;
   b.ldy = H->N;
   b.ctr = ctr;
+  b.plan = PlanArgs{H->st_item[1].as<StageItem>(), H->st_copy[1].as<StageCopy>(), H->st_meta[1].as<StageMeta>()};
   if (L.grid2 > 0) {
-    launch_pdl(k_phase2<NR, WP>, (unsigned)L.grid2, THREADS, G2::smem(true), st, b);
+    launch_pdl(k_phase2<NR, WP, GV2>, (unsigned)L.grid2, THREADS, G2::smem(true), st, b);
     HH_LAUNCHED();
   }
   mark(3);
+}
+
+// the planned single-RHS product runs the stage geometry its plan was built for (hh_matrix::geom)
+template <int NR, int WP = 0>
+void matvec_chunk(hh_matrix *H, const double *x, double *y, int col0, cudaStream_t st) {
+  if constexpr (mv::planned<NR, WP>()) {
+    const int g1 = H->geom[0], g2 = H->geom[1];
+    if (g1 && g2) return matvec_chunk_g<1, 0, 1, 1>(H, x, y, col0, st);
+    if (g1) return matvec_chunk_g<1, 0, 1, 0>(H, x, y, col0, st);
+    if (g2) return matvec_chunk_g<1, 0, 0, 1>(H, x, y, col0, st);
+  }
+  matvec_chunk_g<NR, WP, 0, 0>(H, x, y, col0, st);
 }
 
 template <int WP>
