@@ -113,6 +113,11 @@ enum { HH_STORE_LR = 0, HH_STORE_DENSE = 1 };
  *   precision_set bitmask of HH_P_*, must contain HH_P_FP64; may OR HH_LEDGER_ONLY.
  *   cuda_stream   cudaStream_t (NULL = legacy default stream).  hh_build synchronises it.
  *   out           receives the handle on HH_OK (unchanged otherwise).
+ * Ownership: the handle owns every device allocation it makes — the per-tag factor arenas and
+ * the dense arena (hh_info_t: w_bytes, u_bytes, d_bytes), the block and plan tables, the matvec
+ * workspace ([x~ ; z] for 16 right-hand sides) and the precomputed stage plan of the single-RHS
+ * product (96 bytes per streamed shared-memory stage, about 0.35% of the stored bytes) — until
+ * hh_free.  Nothing is allocated inside hh_matvec.
  * Sketch limit: the device compressor widens a block's randomized sketch until its rank decision
  * provably equals the truncated-SVD decision (G26).  If a block reaches the 4096-column
  * limit (below min(|I|, |J|)) with a decision that is valid (the explicit residual meets eps) but
