@@ -279,6 +279,41 @@ print("row-split ok")
     assert "row-split ok" in out.stdout
 
 
+def test_planned_product_alternative_stage_geometry_matches_oracle():
+    """The single-RHS product streams a stage plan precomputed at hh_build (DESIGN.md §4/§5);
+    its second stage geometry (4 stages of 16 KiB, HH_MV_GEOM1/2 = 1) is an A/B variant of the
+    product build: the same results within 1e-12 of the oracle's Alg. 3 on the exported factors,
+    bitwise reproducible, also through the row-split phase 1 and in every phase combination."""
+    import subprocess
+    import sys
+    code = r'''
+import os, sys
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+import numpy as np, workloads as W, parity_lib as PL
+for name in ("2d_fig8_e4", "3d_small_exp", "3d_sphere_small"):
+    cfg = W.SMALL_CONFIGS[name]
+    P = W.make_points(cfg)
+    H = PL.gpu_build(P, cfg)
+    ex = PL.export(H)
+    lay = PL.check_packing(ex)
+    x = W.make_rhs(cfg, 1)
+    y = PL.gpu_matvec(H, x)
+    assert np.array_equal(y, PL.gpu_matvec(H, x))
+    yo = PL.oracle_matvec_on_export(ex, lay, x)
+    r = PL.rel2(y[:, 0], yo[:, 0])
+    assert r <= 1e-12, (name, r)
+print("geometry ok")
+'''
+    for g1, g2, rows in (("1", "1", None), ("1", "0", None), ("0", "1", None), ("1", "1", "40")):
+        env = dict(os.environ, HH_MV_GEOM1=g1, HH_MV_GEOM2=g2)
+        if rows:
+            env["HH_P1_ROWS"] = rows
+        out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True,
+                             timeout=600)
+        assert out.returncode == 0, out.stdout + out.stderr
+        assert "geometry ok" in out.stdout
+
+
 def test_switch_level_search_matches_oracle():
     """NEXT-2: Alg. 5 (PAPER.md:726-749) on ledger-only builds equals the oracle's walk on its
     own builds — the same ell* and the same storage at every visited level (bits-aware)."""
