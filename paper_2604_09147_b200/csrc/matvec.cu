@@ -950,6 +950,10 @@ __global__ void __launch_bounds__(THREADS, min_ctas<NR, 1>()) k_phase1(P1Args a)
       const int w = tag_bytes(T.tag);
       const int rowb = T.ct * w;
       int rs = max(1, min(G::XELEMS / NR, G::WDATA / rowb));
+      // DMMA K-steps take 4 rows: whole K-steps per window (49 rows of a 248-column fp32 tile
+      // would pad every window's 13th K-step with 3 zero rows, 6% of the issued DMMAs)
+      if constexpr (use_mma<NR>() && WP == 0)
+        if (rs >= 4) rs &= ~3;
       if constexpr (quartered<NR, WP>()) {  // four quarter regions per buffer; whole K-steps per quarter
         int Q = max(1, min(quarter_max_bytes(G::WBUF) / rowb, quarter_max_bytes(G::XBUF) / (NR * 8)));
         if (Q >= 4) Q &= ~3;  // quarters start 16-B aligned alike => exact 8-bank skew
@@ -1473,6 +1477,8 @@ __global__ void __launch_bounds__(THREADS, min_ctas<NR, 2>()) k_phase2(P2Args a)
         const int w = tag_bytes(S.tag);
         const int colb = Lf.nr * w;
         int cs = max(1, min(G::XELEMS / NR, G::WDATA / colb));
+        if constexpr (use_mma<NR>() && WP == 0)  // whole 4-column DMMA K-steps per window
+          if (cs >= 4) cs &= ~3;
         if constexpr (quartered<NR, WP>()) {  // four quarter regions per buffer; whole K-steps per quarter
           int Q = max(1, min(quarter_max_bytes(G::WBUF) / colb, quarter_max_bytes(G::XBUF) / (NR * 8)));
           if (Q >= 4) Q &= ~3;  // quarters start 16-B aligned alike => exact 8-bank skew
